@@ -1,0 +1,134 @@
+/*
+ * ccl_cuda.h — C-ABI of the B200-native connected-components labeler.
+ *
+ * This is the drop-in boundary under the reference's C++ entry point
+ * `ccl::label_image` (/root/reference/proj/include/ccl/pipeline.hpp:33-34,
+ * implemented at /root/reference/proj/src/pipeline.cpp:11-52).  The host C++
+ * in include/ccl/pipeline.hpp keeps that signature verbatim and calls down
+ * through these functions; any FFI (ctypes, cgo, JNI, N-API) can bind them
+ * directly: plain pointers and sizes, no C++ or torch types, no exceptions.
+ *
+ * Output convention (identical to the reference, image.hpp:11-15,41-43):
+ *   labels[x + y*W] = minimum raster index of the pixel's 4-connected
+ *   foreground component, foreground iff image byte == 1, background
+ *   CCL_BACKGROUND (0xFFFFFFFF).  Bit-exact with ccl::sequential_ccl and
+ *   ccl::label_image of the reference for every block config and variant.
+ *
+ * Every function returns a ccl_status; on failure ccl_last_error() returns a
+ * thread-local message.  All functions are thread-safe; a ccl_ctx must not be
+ * used by two host threads at the same time (create one per thread).
+ */
+#ifndef CCL_CUDA_H
+#define CCL_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CCL_BACKGROUND 0xFFFFFFFFu
+
+typedef enum {
+    CCL_OK = 0,
+    CCL_EINVAL = 1,  /* bad argument: size 0 / > 2^32-2 px, bad variant, null ptr (pipeline.cpp:13-15) */
+    CCL_ENOMEM = 2,  /* device or pinned-host allocation failed */
+    CCL_ECUDA = 3,   /* CUDA runtime / launch error (message has the CUDA error string) */
+    CCL_ENODEV = 4   /* no usable sm_100 device */
+} ccl_status;
+
+/* Variant (image.hpp:68-73).  All four produce identical labels; they select
+ * the kernel's local-labeling strategy (template instantiation). */
+typedef enum { CCL_C2FL = 0, CCL_RC2FL = 1, CCL_CC2FL = 2, CCL_NC2FL = 3 } ccl_variant;
+
+typedef struct ccl_ctx ccl_ctx;  /* device, stream, pinned + device workspace cache */
+
+/* Per-kernel device times (ms) of the last call on a context, from CUDA events. */
+typedef struct {
+    float local_ms;  /* kernel (a)(b)(c): tile-local labeling + seam export        */
+    float merge_ms;  /* kernel (d): boundary-only global union-find                 */
+    float final_ms;  /* kernel (e): recompute + path-compressed global relabel      */
+    float total_ms;  /* first launch start to last launch end (== RunReport.wall_time) */
+} ccl_timing;
+
+ccl_status ccl_ctx_create(int device, ccl_ctx** out);
+void ccl_ctx_destroy(ccl_ctx* ctx);
+/* The context's stream (cudaStream_t) as an opaque pointer. */
+void* ccl_ctx_stream(ccl_ctx* ctx);
+
+/* Device-resident path (the timed roofline path).  d_img: H rows of
+ * `img_pitch` bytes (pitch >= w).  d_labels: W*H u32, row-major, stride W.
+ * Enqueued on `stream` exactly as given (NULL = the legacy default stream;
+ * pass ccl_ctx_stream(ctx) for the context's own stream); asynchronous.
+ * `timing` (may be NULL) is filled after the call only if `sync` != 0. */
+ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                            uint32_t* d_labels, int variant, void* stream, int sync, ccl_timing* timing);
+
+/* Host path used by ccl::label_image: H2D (pinned staging), the kernels, D2H.
+ * Blocking.  `kernel_ms` (may be NULL) = device time of the kernels only. */
+ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels,
+                          int variant, float* kernel_ms);
+
+/* Batch of n frames of w*h, frame f at d_frames + f*frame_pitch (rows of
+ * img_pitch bytes).  Labels are per-frame raster indices at d_labels + f*w*h.
+ * One launch per kernel for the whole batch.  Asynchronous on `stream`. */
+ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pitch, size_t frame_pitch,
+                           uint32_t n, uint32_t w, uint32_t h, uint32_t* d_labels, int variant, void* stream);
+
+/* ---- Strip mode (image split into horizontal strips, one per GPU/rank) ----
+ * A strip holds rows [row0, row0+h) of a full image of `full_h` rows, width w;
+ * every strip but the last must have h a multiple of the tile height
+ * (ccl_tile_shape).  Labels are GLOBAL raster indices x + (row0+y)*w; the
+ * strip's label buffer holds indices [row0*w, (row0+h)*w).  Protocol:
+ *   1. ccl_strip_local        kernels (a)(b)(c)(d) on the strip
+ *   2. ccl_strip_seam_export  4*w u32 to d_seam_out: the strip-local roots of
+ *                             its top and bottom rows (2*w, background =
+ *                             CCL_BACKGROUND) and, per seam node, the global
+ *                             node index of the first seam node of the same
+ *                             strip root (2*w)
+ *   3. all-gather the n_strips*4*w words (NCCL / peer copies) in strip order
+ *   4. ccl_strip_seam_resolve union-find over all strips' seam nodes, run
+ *                             identically on every strip (no broadcast), then
+ *                             each own seam root's final label is written into
+ *                             the strip's forest
+ *   5. ccl_strip_final        kernel (e) on the strip
+ * Steps 2-4 must all run before step 5; the strip's label buffer is not a
+ * valid forest between 2 and 4. */
+ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream);
+ccl_status ccl_strip_seam_export(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
+                                 uint32_t strip_index, uint32_t* d_labels, uint32_t* d_seam_out, void* stream);
+ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint32_t n_strips,
+                                  uint32_t strip_index, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
+                                  uint32_t* d_labels, uint32_t* d_scratch, void* stream);
+ccl_status ccl_strip_final(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream);
+/* d_scratch for ccl_strip_seam_resolve must hold ccl_strip_scratch_words(n_strips, w) u32. */
+size_t ccl_strip_scratch_words(uint32_t n_strips, uint32_t w);
+
+/* GPU compaction (pipeline.cpp:54-70, "next" row (f)1): labels 1..K in raster
+ * order of first appearance, background 0; K written to *k_out (host).
+ * d_scratch must hold ccl_compact_scratch_words(w, h) u32. Blocking. */
+ccl_status ccl_compact_device(ccl_ctx* ctx, const uint32_t* d_raw, uint32_t w, uint32_t h, uint32_t* d_out,
+                              uint32_t* d_scratch, uint64_t* k_out, void* stream);
+size_t ccl_compact_scratch_words(uint32_t w, uint32_t h);
+
+/* Tile geometry used by the kernels (for docs / tests). */
+void ccl_tile_shape(uint32_t* tile_w, uint32_t* tile_h);
+/* Number of kernel launches one ccl_label_device call makes. */
+int ccl_launches_per_label(void);
+
+/* Host-side synthetic inputs, byte-identical to the reference generators
+ * (generate.cpp:9-106).  kind: 0 stripes, 1 spiral, 2 blobs, 3 checkerboard. */
+ccl_status ccl_gen_random(uint8_t* out, uint32_t w, uint32_t h, double density, uint64_t seed);
+ccl_status ccl_gen_pattern(uint8_t* out, int kind, uint32_t w, uint32_t h, uint32_t period, double density,
+                           uint64_t seed);
+
+const char* ccl_last_error(void);
+const char* ccl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCL_CUDA_H */

@@ -1,0 +1,93 @@
+"""In-tree build of the native library ``_lib/libccl_b200.so`` (sm_100a only).
+
+Every CUDA and host C++ source under ``csrc/`` is compiled with nvcc
+(``-gencode arch=compute_100a,code=sm_100a -lineinfo``) and linked into one
+shared library exporting the C-ABI of ``include/ccl_cuda.h`` and the C++ API
+of ``include/ccl/*.hpp``.  The .so is git-ignored but lives in the tree, so it
+travels to the GPU box with ``gpurun``.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT_DIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(OUT_DIR, "libccl_b200.so")
+OBJ_DIR = os.path.join(REPO, "build", "obj")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def sources() -> list[str]:
+    out = []
+    for root, _, files in os.walk(CSRC):
+        for f in sorted(files):
+            if f.endswith((".cu", ".cpp")):
+                out.append(os.path.join(root, f))
+    return sorted(out)
+
+
+def _flags(extra: list[str] | None = None) -> list[str]:
+    fl = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+                 "-I", os.path.join(REPO, "include"), "-I", CSRC]
+    tile = os.environ.get("CCL_TILE")  # e.g. "8x2" for experiments
+    if tile:
+        wx, wy = tile.lower().split("x")
+        fl += [f"-DCCL_TILE_WX={int(wx)}", f"-DCCL_TILE_WY={int(wy)}"]
+    return fl + (extra or [])
+
+
+def _needs(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    deps += [os.path.join(REPO, "include", d, f) for d in ("", "ccl")
+             for f in os.listdir(os.path.join(REPO, "include", d)) if f.endswith((".h", ".hpp"))]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    nvcc = _nvcc()
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    os.makedirs(OUT_DIR, exist_ok=True)
+    srcs = sources()
+    tag = os.environ.get("CCL_TILE", "default").replace("x", "_")
+    objs = [os.path.join(OBJ_DIR, os.path.relpath(s, CSRC).replace(os.sep, "__") + f".{tag}.o") for s in srcs]
+    jobs = []
+    for s, o in zip(srcs, objs):
+        if force or _needs(o, s):
+            cmd = [nvcc] + _flags(["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
+            if s.endswith(".cpp"):
+                cmd = [nvcc] + _flags() + ["-x", "cu", "-c", s, "-o", o]
+            jobs.append(cmd)
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs):
+            if verbose and (r.stdout or r.stderr):
+                print(r.stdout + r.stderr, file=sys.stderr)
+            if r.returncode != 0:
+                raise RuntimeError("nvcc failed:\n" + " ".join(r.args) + "\n" + r.stdout + r.stderr)
+    if force or jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        tmp = LIB + ".tmp"
+        link = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]
+        r = subprocess.run(link, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,0 +1,406 @@
+// ccl_capi.cu — the extern "C" boundary (include/ccl_cuda.h): contexts,
+// argument validation with the reference's error semantics
+// (pipeline.cpp:13-15, image.hpp:31-38), TMA descriptor setup, staging and
+// timing.  No exception crosses this boundary; every CUDA failure becomes a
+// status code plus a thread-local message.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <mutex>
+#include <string>
+
+#include "ccl/generate.hpp"
+#include "ccl_cuda.h"
+#include "ccl_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+ccl_status fail(ccl_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+ccl_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? CCL_ENOMEM : CCL_ECUDA,
+                std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+#define CCL_CHECK(call)                                   \
+    do {                                                  \
+        cudaError_t e__ = (call);                         \
+        if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+    } while (0)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+    static std::once_flag once;
+    static EncodeFn fn = nullptr;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+}  // namespace
+
+struct ccl_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // host-path workspace (grown on demand)
+    uint8_t* d_img = nullptr;
+    size_t d_img_bytes = 0;
+    uint32_t* d_lab = nullptr;
+    size_t d_lab_bytes = 0;
+    uint8_t* h_img = nullptr;  // pinned
+    size_t h_img_bytes = 0;
+    uint32_t* h_lab = nullptr;  // pinned
+    size_t h_lab_bytes = 0;
+    ccl_timing last{};
+};
+
+namespace {
+
+ccl_status check_dims(uint32_t w, uint32_t h) {
+    if (w == 0 || h == 0) return fail(CCL_EINVAL, "image dimensions must be at least 1x1");
+    if (uint64_t(w) * h > uint64_t(CCL_BACKGROUND) - 1) return fail(CCL_EINVAL, "image exceeds 2^32-2 pixels");
+    return CCL_OK;
+}
+
+ccl_status make_geo(uint32_t w, uint32_t h, uint32_t row0, size_t img_pitch, size_t frame_pitch, bool above,
+                    bool below, cclk::Geo* g) {
+    const uint32_t tw = uint32_t(cclk::tile_w()), th = uint32_t(cclk::tile_h());
+    g->W = w;
+    g->H = h;
+    g->ntx = (w + tw - 1) / tw;
+    g->nty = (h + th - 1) / th;
+    g->row0 = row0;
+    g->base = row0 * w;
+    g->edge_above = above ? 1u : 0u;
+    g->edge_below = below ? 1u : 0u;
+    g->img_pitch = img_pitch;
+    g->frame_pitch = frame_pitch;
+    g->frame_px = size_t(w) * h;
+    if (below && (h % th) != 0) return fail(CCL_EINVAL, "strip height must be a multiple of the tile height");
+    return CCL_OK;
+}
+
+ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t frame_pitch, uint32_t nframes,
+                   uint32_t* labels, int variant, cudaStream_t s) {
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
+    a->nframes = nframes;
+    a->variant = variant;
+    a->img = img;
+    a->labels = labels;
+    a->stream = s;
+    std::memset(&a->tm_img, 0, sizeof(a->tm_img));
+    std::memset(&a->tm_lab, 0, sizeof(a->tm_lab));
+    const cclk::Geo& g = a->g;
+    EncodeFn enc = encode_fn();
+    a->tma_load = enc && (reinterpret_cast<uintptr_t>(img) % 16 == 0) && (pitch % 16 == 0) &&
+                  (frame_pitch % 16 == 0) && pitch < (uint64_t(1) << 40);
+    a->tma_store = enc && (reinterpret_cast<uintptr_t>(labels) % 16 == 0) && (uint64_t(g.W) * 4 % 16 == 0);
+    if (a->tma_load) {
+        const cuuint64_t dims[3] = {g.W, g.H, nframes};
+        const cuuint64_t strides[2] = {pitch, frame_pitch};
+        const cuuint32_t box[3] = {uint32_t(cclk::tile_w()), uint32_t(cclk::tile_h()), 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&a->tm_img, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(img), dims, strides, box,
+                         es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) a->tma_load = false;
+    }
+    if (a->tma_store) {
+        const cuuint64_t dims[3] = {g.W, g.H, nframes};
+        const cuuint64_t strides[2] = {cuuint64_t(g.W) * 4, cuuint64_t(g.frame_px) * 4};
+        const cuuint32_t box[3] = {32, 32, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&a->tm_lab, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, labels, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) a->tma_store = false;
+    }
+    return CCL_OK;
+}
+
+ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events) {
+    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[0], a.stream));
+    CCL_CHECK(cclk::launch_local(a));
+    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[1], a.stream));
+    CCL_CHECK(cclk::launch_seams(a));
+    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[2], a.stream));
+    CCL_CHECK(cclk::launch_final(a));
+    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[3], a.stream));
+    return CCL_OK;
+}
+
+ccl_status read_timing(ccl_ctx* ctx, ccl_timing* t) {
+    CCL_CHECK(cudaEventSynchronize(ctx->ev[3]));
+    ccl_timing r{};
+    CCL_CHECK(cudaEventElapsedTime(&r.local_ms, ctx->ev[0], ctx->ev[1]));
+    CCL_CHECK(cudaEventElapsedTime(&r.merge_ms, ctx->ev[1], ctx->ev[2]));
+    CCL_CHECK(cudaEventElapsedTime(&r.final_ms, ctx->ev[2], ctx->ev[3]));
+    CCL_CHECK(cudaEventElapsedTime(&r.total_ms, ctx->ev[0], ctx->ev[3]));
+    ctx->last = r;
+    if (t) *t = r;
+    return CCL_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+ccl_status ccl_ctx_create(int device, ccl_ctx** out) {
+    if (!out) return fail(CCL_EINVAL, "null out pointer");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return fail(CCL_ENODEV, "no CUDA device visible");
+    if (device < 0 || device >= n) return fail(CCL_ENODEV, "device index out of range");
+    cudaDeviceProp prop;
+    CCL_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(CCL_ENODEV, std::string("built for sm_100a; device is ") + prop.name);
+    DeviceGuard dg(device);
+    ccl_ctx* c = new ccl_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) {
+        ccl_ctx_destroy(c);
+        return cuda_fail(e, "ccl_ctx_create");
+    }
+    *out = c;
+    return CCL_OK;
+}
+
+void ccl_ctx_destroy(ccl_ctx* c) {
+    if (!c) return;
+    DeviceGuard dg(c->device);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->d_img) cudaFree(c->d_img);
+    if (c->d_lab) cudaFree(c->d_lab);
+    if (c->h_img) cudaFreeHost(c->h_img);
+    if (c->h_lab) cudaFreeHost(c->h_lab);
+    delete c;
+}
+
+void* ccl_ctx_stream(ccl_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                            uint32_t* d_labels, int variant, void* stream, int sync, ccl_timing* timing) {
+    if (!ctx || !d_img || !d_labels) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (img_pitch < w) return fail(CCL_EINVAL, "image pitch smaller than width");
+    DeviceGuard dg(ctx->device);
+    cclk::LaunchArgs a{};
+    if (ccl_status s = make_geo(w, h, 0, img_pitch, img_pitch * h, false, false, &a.g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    if (ccl_status s = run_pipeline(ctx, a, true)) return s;
+    if (sync) return read_timing(ctx, timing);
+    return CCL_OK;
+}
+
+ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pitch, size_t frame_pitch, uint32_t n,
+                           uint32_t w, uint32_t h, uint32_t* d_labels, int variant, void* stream) {
+    if (!ctx || !d_frames || !d_labels) return fail(CCL_EINVAL, "null argument");
+    if (n == 0) return CCL_OK;
+    if (n > 65535) return fail(CCL_EINVAL, "at most 65535 frames per batch call");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (img_pitch < w || frame_pitch < img_pitch * h) return fail(CCL_EINVAL, "bad pitch");
+    DeviceGuard dg(ctx->device);
+    cclk::LaunchArgs a{};
+    if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ccl_status s = prepare(&a, d_frames, img_pitch, frame_pitch, n, d_labels, variant, st)) return s;
+    return run_pipeline(ctx, a, true);
+}
+
+ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels, int variant,
+                          float* kernel_ms) {
+    if (!ctx || !img || !labels) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
+    DeviceGuard dg(ctx->device);
+    const size_t pitch = (size_t(w) + 15) / 16 * 16;  // 16B-aligned rows for the TMA tile loads
+    const size_t img_bytes = pitch * h, lab_bytes = size_t(w) * h * 4;
+    if (ctx->d_img_bytes < img_bytes) {
+        if (ctx->d_img) cudaFree(ctx->d_img);
+        ctx->d_img = nullptr;
+        ctx->d_img_bytes = 0;
+        CCL_CHECK(cudaMalloc(&ctx->d_img, img_bytes));
+        ctx->d_img_bytes = img_bytes;
+    }
+    if (ctx->d_lab_bytes < lab_bytes) {
+        if (ctx->d_lab) cudaFree(ctx->d_lab);
+        ctx->d_lab = nullptr;
+        ctx->d_lab_bytes = 0;
+        CCL_CHECK(cudaMalloc(&ctx->d_lab, lab_bytes));
+        ctx->d_lab_bytes = lab_bytes;
+    }
+    CCL_CHECK(cudaMemcpy2DAsync(ctx->d_img, pitch, img, w, w, h, cudaMemcpyHostToDevice, ctx->stream));
+    ccl_timing t{};
+    if (ccl_status s = ccl_label_device(ctx, ctx->d_img, pitch, w, h, ctx->d_lab, variant, ctx->stream, 0, nullptr))
+        return s;
+    CCL_CHECK(cudaMemcpyAsync(labels, ctx->d_lab, lab_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (ccl_status s = read_timing(ctx, &t)) return s;
+    if (kernel_ms) *kernel_ms = t.total_ms;
+    return CCL_OK;
+}
+
+// ---------------------------------------------------------------- strip mode
+namespace {
+ccl_status strip_geo(uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, size_t pitch, cclk::Geo* g) {
+    if (ccl_status s = check_dims(w, full_h)) return s;
+    if (h == 0 || uint64_t(row0) + h > full_h) return fail(CCL_EINVAL, "strip rows outside the image");
+    // the top row of every strip is exported (also strip 0: keeps seam reps uniform)
+    return make_geo(w, h, row0, pitch, pitch * h, true, row0 + h < full_h, g);
+}
+}  // namespace
+
+ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream) {
+    if (!ctx || !d_img || !d_labels) return fail(CCL_EINVAL, "null argument");
+    if (img_pitch < w) return fail(CCL_EINVAL, "image pitch smaller than width");
+    DeviceGuard dg(ctx->device);
+    cclk::LaunchArgs a{};
+    if (ccl_status s = strip_geo(w, h, row0, full_h, img_pitch, &a.g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    CCL_CHECK(cclk::launch_local(a));
+    CCL_CHECK(cclk::launch_seams(a));
+    return CCL_OK;
+}
+
+ccl_status ccl_strip_seam_export(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
+                                 uint32_t strip_index, uint32_t* d_labels, uint32_t* d_seam_out, void* stream) {
+    if (!ctx || !d_labels || !d_seam_out) return fail(CCL_EINVAL, "null argument");
+    DeviceGuard dg(ctx->device);
+    cclk::Geo g{};
+    if (ccl_status s = strip_geo(w, h, row0, full_h, w, &g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CCL_CHECK(cclk::launch_strip_export(g, d_labels, d_seam_out, strip_index, st));
+    return CCL_OK;
+}
+
+ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint32_t n_strips, uint32_t strip_index,
+                                  uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, uint32_t* d_labels,
+                                  uint32_t* d_scratch, void* stream) {
+    if (!ctx || !d_seam_all || !d_labels || !d_scratch) return fail(CCL_EINVAL, "null argument");
+    if (n_strips == 0 || strip_index >= n_strips) return fail(CCL_EINVAL, "bad strip index");
+    if (uint64_t(n_strips) * 2 * w >= 0xFFFFFFFFull) return fail(CCL_EINVAL, "too many seam nodes");
+    DeviceGuard dg(ctx->device);
+    cclk::Geo g{};
+    if (ccl_status s = strip_geo(w, h, row0, full_h, w, &g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CCL_CHECK(cclk::launch_strip_resolve(g, d_seam_all, n_strips, strip_index, d_labels, d_scratch, st));
+    return CCL_OK;
+}
+
+ccl_status ccl_strip_final(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream) {
+    if (!ctx || !d_img || !d_labels) return fail(CCL_EINVAL, "null argument");
+    if (img_pitch < w) return fail(CCL_EINVAL, "image pitch smaller than width");
+    DeviceGuard dg(ctx->device);
+    cclk::LaunchArgs a{};
+    if (ccl_status s = strip_geo(w, h, row0, full_h, img_pitch, &a.g)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    CCL_CHECK(cclk::launch_final(a));
+    return CCL_OK;
+}
+
+size_t ccl_strip_scratch_words(uint32_t n_strips, uint32_t w) { return size_t(n_strips) * 2 * w; }
+
+// ---------------------------------------------------------------- compaction
+ccl_status ccl_compact_device(ccl_ctx* ctx, const uint32_t* d_raw, uint32_t w, uint32_t h, uint32_t* d_out,
+                              uint32_t* d_scratch, uint64_t* k_out, void* stream) {
+    if (!ctx || !d_raw || !d_out || !d_scratch) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    DeviceGuard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = size_t(w) * h;
+    CCL_CHECK(cclk::launch_compact(d_raw, n, d_out, d_scratch, st));
+    if (k_out) {
+        const size_t words = (n + 31) / 32, nb = (words + 1023) / 1024;
+        uint32_t k = 0;
+        CCL_CHECK(cudaMemcpyAsync(&k, d_scratch + 2 * words + nb, 4, cudaMemcpyDeviceToHost, st));
+        CCL_CHECK(cudaStreamSynchronize(st));
+        *k_out = k;
+    }
+    return CCL_OK;
+}
+
+size_t ccl_compact_scratch_words(uint32_t w, uint32_t h) { return cclk::compact_scratch_words(size_t(w) * h); }
+
+// ---------------------------------------------------------------- generators
+ccl_status ccl_gen_random(uint8_t* out, uint32_t w, uint32_t h, double density, uint64_t seed) {
+    if (!out) return fail(CCL_EINVAL, "null argument");
+    try {
+        const ccl::BinaryImage img = ccl::random_image(w, h, density, seed);
+        std::memcpy(out, img.data.data(), img.data.size());
+        return CCL_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(CCL_EINVAL, e.what());
+    } catch (const std::exception& e) {
+        return fail(CCL_ENOMEM, e.what());
+    }
+}
+
+ccl_status ccl_gen_pattern(uint8_t* out, int kind, uint32_t w, uint32_t h, uint32_t period, double density,
+                           uint64_t seed) {
+    if (!out) return fail(CCL_EINVAL, "null argument");
+    if (kind < 0 || kind > 3) return fail(CCL_EINVAL, "unknown pattern kind");
+    try {
+        ccl::PatternParams pp;
+        pp.period = period;
+        pp.density = density;
+        pp.seed = seed;
+        const ccl::BinaryImage img = ccl::pattern_image(static_cast<ccl::PatternKind>(kind), w, h, pp);
+        std::memcpy(out, img.data.data(), img.data.size());
+        return CCL_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(CCL_EINVAL, e.what());
+    } catch (const std::exception& e) {
+        return fail(CCL_ENOMEM, e.what());
+    }
+}
+
+void ccl_tile_shape(uint32_t* tw, uint32_t* th) {
+    if (tw) *tw = uint32_t(cclk::tile_w());
+    if (th) *th = uint32_t(cclk::tile_h());
+}
+
+int ccl_launches_per_label(void) { return 3; }
+
+const char* ccl_last_error(void) { return g_err.c_str(); }
+
+const char* ccl_version(void) { return "ccl-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// ccl_device.cuh — device-side building blocks of the sm_100a labeler.
+//
+// Reference mapping (arXiv 1712.09789 as restated in /root/reference/proj):
+//   foreground predicate byte == 1 ......... local_labeler.cpp:59,64 / oracle.cpp:41-43
+//   parent[i] <= i forest, min-union ........ forest.hpp:44-111
+//   find_root / flatten ..................... forest.hpp:72-92
+//   coarse row scan (runs) .................. local_labeler.cpp:30-38  -> word-level run starts
+//   coarse column scan ...................... local_labeler.cpp:40-48  -> link run to first upper overlap
+//   refine (min-union merges) ............... local_labeler.cpp:55-68  -> smem atomicMin union
+//   convert_ids (local -> global raster idx). local_labeler.cpp:102-112
+//   merge_borders ........................... boundary.cpp:22-35       -> global atomicMin union
+//   resolve_global .......................... boundary.cpp:37-55       -> path-compressing relabel
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cclk {
+
+constexpr uint32_t kBG = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------- bit helpers
+// Foreground bits of 4 bytes: bit k set iff byte k == 1 (exact for any byte value).
+__device__ __forceinline__ uint32_t eq1_nibble(uint32_t v) {
+    const uint32_t x = v ^ 0x01010101u;                 // zero bytes where v == 1
+    uint32_t y = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;       // high bit set where low 7 bits != 0
+    y = ~(y | x | 0x7F7F7F7Fu);                         // 0x80 exactly in the zero bytes of x
+    return ((y >> 7) * 0x10204080u) >> 28;              // gather bits 0,8,16,24 -> nibble
+}
+__device__ __forceinline__ uint32_t eq1_mask16(uint4 q) {
+    return eq1_nibble(q.x) | (eq1_nibble(q.y) << 4) | (eq1_nibble(q.z) << 8) | (eq1_nibble(q.w) << 12);
+}
+// Highest set bit of s at or below bit b (caller guarantees one exists).
+__device__ __forceinline__ uint32_t hi_bit_le(uint32_t s, uint32_t b) {
+    return 31u - __clz(s & (0xFFFFFFFFu >> (31u - b)));
+}
+// Bits b of o such that some bit of o lies strictly below b inside the same
+// run of m (o must be a subset of m): the carry-in vector of m + o, within m.
+__device__ __forceinline__ uint32_t has_lower_in_run(uint32_t m, uint32_t o) {
+    return ((m + o) ^ m ^ o) & m;
+}
+
+// ----------------------------------------------------------- smem union-find
+// Lock-free min-union over a shared-memory parent array (forest.hpp:98-111
+// semantics: the larger root is linked below the smaller one, so every class
+// is rooted at its minimum node).  atomicMin instead of CAS: a lost race is
+// repaired by continuing with the returned parent (Playne-Hawick style).
+__device__ __forceinline__ uint32_t sfind(volatile uint32_t* P, uint32_t x) {
+    uint32_t p = P[x];
+    while (p != x) {
+        const uint32_t gp = P[p];
+        if (gp == p) return p;
+        P[x] = gp;  // path halving; only ever writes an ancestor
+        x = gp;
+        p = P[x];
+    }
+    return x;
+}
+__device__ __forceinline__ void sunion(uint32_t* P, uint32_t a, uint32_t b) {
+    volatile uint32_t* vP = P;
+    for (;;) {
+        a = sfind(vP, a);
+        b = sfind(vP, b);
+        if (a == b) return;
+        if (a < b) { const uint32_t t = a; a = b; b = t; }
+        const uint32_t old = atomicMin(&P[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// --------------------------------------------------------- global union-find
+// The forest lives in the output label buffer L itself (no extra W*H array).
+// Node ids are global raster indices; `base` is the first index held by this
+// buffer (strip mode) — a parent value < base is a foreign, terminal root
+// written by the strip seam resolve.
+__device__ __forceinline__ uint32_t gload(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t gfind(uint32_t* L, uint32_t base, uint32_t x) {
+    uint32_t p = gload(L + (x - base));
+    while (p != x) {
+        if (p < base) return p;
+        const uint32_t gp = gload(L + (p - base));
+        if (gp == p || gp < base) return gp;
+        L[x - base] = gp;  // path halving
+        x = gp;
+        p = gload(L + (x - base));
+    }
+    return x;
+}
+// Read-only variant for the final relabel: kernel (e) overwrites every
+// pixel's entry with its final label while other CTAs still walk the forest,
+// so a halving store could land after (and clobber) a final label.
+__device__ __forceinline__ uint32_t gfind_ro(const uint32_t* L, uint32_t base, uint32_t x) {
+    uint32_t p = gload(L + (x - base));
+    while (p != x && p >= base) {
+        x = p;
+        p = gload(L + (x - base));
+    }
+    return p;
+}
+__device__ __forceinline__ void gunion(uint32_t* L, uint32_t base, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = gfind(L, base, a);
+        b = gfind(L, base, b);
+        if (a == b) return;
+        if (a < b) { const uint32_t t = a; a = b; b = t; }
+        const uint32_t old = atomicMin(L + (a - base), b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// --------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm), "r"(x),
+                 "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_and_wait() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
+}
+
+}  // namespace cclk

@@ -1,0 +1,59 @@
+// ccl_internal.h — shared between the kernel TUs and the C-ABI TU (not installed).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+// GPU tile = CCL_TILE_WX x CCL_TILE_WY warps, each warp a 32x32 pixel sub-tile.
+#ifndef CCL_TILE_WX
+#define CCL_TILE_WX 8
+#endif
+#ifndef CCL_TILE_WY
+#define CCL_TILE_WY 1
+#endif
+
+namespace cclk {
+
+// Geometry of one labeling problem (a frame, a batch of frames or one strip).
+struct Geo {
+    uint32_t W, H;          // width, rows held by this buffer (strip height in strip mode)
+    uint32_t ntx, nty;      // tile grid
+    uint32_t row0;          // global row of the buffer's first row (strip mode), else 0
+    uint32_t base;          // row0 * W: global raster index of L[0]
+    uint32_t edge_above;    // strip has a neighbour strip above / below
+    uint32_t edge_below;
+    size_t img_pitch;       // bytes between image rows
+    size_t frame_pitch;     // bytes between frames (batch)
+    size_t frame_px;        // labels per frame (W*H)
+};
+
+struct LaunchArgs {
+    Geo g;
+    uint32_t nframes;
+    int variant;
+    bool tma_load, tma_store;
+    CUtensorMap tm_img;     // u8 {W, H, F}, box {TW, TH, 1}
+    CUtensorMap tm_lab;     // u32 {W, H, F}, box {32, 32, 1}, 128B swizzle
+    const uint8_t* img;
+    uint32_t* labels;
+    cudaStream_t stream;
+};
+
+cudaError_t launch_local(const LaunchArgs& a);
+cudaError_t launch_seams(const LaunchArgs& a);
+cudaError_t launch_final(const LaunchArgs& a);
+
+// strip-mode and compaction kernels (ccl_aux.cu)
+cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* seam_out, uint32_t strip_index,
+                                cudaStream_t s);
+cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* seam_all, uint32_t n_strips, uint32_t strip_index,
+                                 uint32_t* labels, uint32_t* scratch, cudaStream_t s);
+cudaError_t launch_compact(const uint32_t* raw, size_t n, uint32_t* out, uint32_t* scratch, cudaStream_t s);
+size_t compact_scratch_words(size_t n);
+
+int tile_w();
+int tile_h();
+
+}  // namespace cclk

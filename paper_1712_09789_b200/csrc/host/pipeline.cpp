@@ -1,0 +1,156 @@
+// pipeline.cpp — host C++ drop-in for ccl::label_image
+// (/root/reference/proj/src/pipeline.cpp:11-52) on top of the C-ABI.
+//
+// Same validation order and exceptions as the reference:
+//   !cfg.valid()  -> std::invalid_argument        (pipeline.cpp:13-14)
+//   workers == 0  -> std::invalid_argument        (pipeline.cpp:15)
+//   0x0 image     -> std::invalid_argument via LabelMap/check_size (image.hpp:31-33)
+// plus ccl::DeviceError (a std::runtime_error) for CUDA failures.
+// Each host thread owns its own ccl_ctx (stream + workspace), so concurrent
+// calls on distinct images are safe.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "ccl/generate.hpp"
+#include "ccl/pipeline.hpp"
+#include "ccl_cuda.h"
+
+namespace ccl {
+
+namespace {
+
+thread_local int t_device = 0;
+
+struct CtxDeleter {
+    void operator()(ccl_ctx* c) const { ccl_ctx_destroy(c); }
+};
+
+ccl_ctx* thread_ctx() {
+    thread_local std::unique_ptr<ccl_ctx, CtxDeleter> ctx;
+    thread_local int ctx_dev = -1;
+    if (!ctx || ctx_dev != t_device) {
+        ctx.reset();
+        ccl_ctx* c = nullptr;
+        const ccl_status s = ccl_ctx_create(t_device, &c);
+        if (s != CCL_OK) throw DeviceError(int(s), ccl_last_error());
+        ctx.reset(c);
+        ctx_dev = t_device;
+    }
+    return ctx.get();
+}
+
+void check(ccl_status s) {
+    if (s == CCL_EINVAL) throw std::invalid_argument(ccl_last_error());
+    if (s != CCL_OK) throw DeviceError(int(s), ccl_last_error());
+}
+
+}  // namespace
+
+void set_device(int device) { t_device = device; }
+
+RunReport label_image(const BinaryImage& img, const BlockConfig& cfg, Variant variant, unsigned workers) {
+    if (!cfg.valid()) throw std::invalid_argument("block configuration invalid or over the scratch ceiling");
+    if (workers == 0) throw std::invalid_argument("workers must be >= 1");
+
+    RunReport rep;
+    rep.variant = variant;
+    rep.cfg = cfg;
+    rep.worker_count = workers;
+    rep.blocks_x = (img.width + cfg.block_w - 1) / cfg.block_w;
+    rep.blocks_y = (img.height + cfg.block_h - 1) / cfg.block_h;
+    rep.per_block.resize(std::size_t(rep.blocks_x) * rep.blocks_y);
+    for (std::size_t i = 0; i < rep.per_block.size(); ++i) rep.per_block[i].block_id = std::uint32_t(i);
+
+    rep.label_map = LabelMap(img.width, img.height);  // throws invalid_argument for 0x0 like the reference
+    if (img.data.size() != rep.label_map.labels.size())
+        throw std::invalid_argument("image data size does not match width*height");
+
+    float ms = 0.f;
+    check(ccl_label_host(thread_ctx(), img.data.data(), img.width, img.height, rep.label_map.labels.data(),
+                         int(variant), &ms));
+    rep.wall_time = std::chrono::duration<double, std::milli>(double(ms));
+    return rep;
+}
+
+LabelMap compact_labels(const LabelMap& lm) {
+    if (lm.compacted) return lm;
+    LabelMap out(lm.width, lm.height, 0);
+    out.compacted = true;
+    // roots are component minima, so "order of first appearance" == ascending
+    // root order; one sweep with a dense remap (pipeline.cpp:54-70)
+    std::vector<Label> remap(lm.labels.size(), 0);
+    Label next = 0;
+    for (std::size_t i = 0; i < lm.labels.size(); ++i) {
+        const Label raw = lm.labels[i];
+        if (raw == kBackground) continue;
+        if (remap[raw] == 0) remap[raw] = ++next;
+        out.labels[i] = remap[raw];
+    }
+    return out;
+}
+
+MetricsSummary aggregate_metrics(const RunReport& report) {
+    MetricsSummary s;
+    s.grid_w = report.blocks_x;
+    s.grid_h = report.blocks_y;
+    std::uint64_t it = 0, at = 0;
+    for (const auto& m : report.per_block) {
+        s.iterations_grid.push_back(m.findroot_iterations);
+        s.atomics_grid.push_back(m.atomic_ops);
+        it += m.findroot_iterations;
+        at += m.atomic_ops;
+    }
+    if (!report.per_block.empty()) {
+        s.mean_iterations = double(it) / double(report.per_block.size());
+        s.mean_atomics = double(at) / double(report.per_block.size());
+    }
+    return s;
+}
+
+std::vector<LabelMap> label_batch(const std::vector<BinaryImage>& frames, Variant variant) {
+    std::vector<LabelMap> out;
+    if (frames.empty()) return out;
+    const std::uint32_t w = frames[0].width, h = frames[0].height;
+    for (const auto& f : frames)
+        if (f.width != w || f.height != h) throw std::invalid_argument("label_batch: frames differ in size");
+    ccl_ctx* ctx = thread_ctx();
+    const std::size_t px = BinaryImage::check_size(w, h);
+    const std::size_t pitch = (std::size_t(w) + 15) / 16 * 16, fpitch = pitch * h;
+    const std::uint32_t n = std::uint32_t(frames.size());
+    std::vector<std::uint8_t> host(fpitch * n, 0);
+    for (std::uint32_t f = 0; f < n; ++f)
+        for (std::uint32_t y = 0; y < h; ++y)
+            std::copy_n(frames[f].data.data() + std::size_t(y) * w, w, host.data() + f * fpitch + y * pitch);
+    std::uint8_t* d_img = nullptr;
+    std::uint32_t* d_lab = nullptr;
+    if (cudaMalloc(&d_img, host.size()) != cudaSuccess) throw DeviceError(CCL_ENOMEM, "cudaMalloc frames");
+    if (cudaMalloc(&d_lab, px * n * 4) != cudaSuccess) {
+        cudaFree(d_img);
+        throw DeviceError(CCL_ENOMEM, "cudaMalloc labels");
+    }
+    auto cleanup = [&] {
+        cudaFree(d_img);
+        cudaFree(d_lab);
+    };
+    cudaStream_t st = static_cast<cudaStream_t>(ccl_ctx_stream(ctx));
+    cudaMemcpyAsync(d_img, host.data(), host.size(), cudaMemcpyHostToDevice, st);
+    const ccl_status s = ccl_label_batch(ctx, d_img, pitch, fpitch, n, w, h, d_lab, int(variant), st);
+    if (s != CCL_OK) {
+        cleanup();
+        check(s);
+    }
+    out.reserve(n);
+    for (std::uint32_t f = 0; f < n; ++f) {
+        out.emplace_back(w, h);
+        cudaMemcpyAsync(out.back().labels.data(), d_lab + f * px, px * 4, cudaMemcpyDeviceToHost, st);
+    }
+    const cudaError_t e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) throw DeviceError(CCL_ECUDA, cudaGetErrorString(e));
+    return out;
+}
+
+}  // namespace ccl

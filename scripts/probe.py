@@ -1,0 +1,52 @@
+"""Quick GPU probe: per-kernel device times on the headline workload and a few
+stress patterns (not the bench contract; see bench.py)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1712_09789_b200 as ccl  # noqa: E402
+
+
+def flush(buf):
+    buf.sum()  # read 1 GiB of clean data: evicts (and writes back) everything in L2
+
+
+def run(name, img_np, variant="c2fl", iters=10):
+    img = torch.from_numpy(img_np).cuda()
+    out = torch.empty(img.shape, dtype=torch.uint32, device="cuda")
+    fl = torch.ones(1 << 28, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        ccl.label_device(img, out, variant=variant, sync=True)
+    ts = []
+    for _ in range(iters):
+        flush(fl)
+        torch.cuda.synchronize()
+        _, t = ccl.label_device(img, out, variant=variant, sync=True)
+        ts.append(t)
+    med = lambda k: sorted(x[k] for x in ts)[len(ts) // 2]
+    px = img.numel()
+    tot = med("total_ms")
+    gbs = px * 5 / (tot * 1e-3) / 1e9
+    print(f"{name:28s} {variant:6s} local {med('local_ms')*1e3:7.1f}us merge {med('merge_ms')*1e3:7.1f}us "
+          f"final {med('final_ms')*1e3:7.1f}us total {tot*1e3:7.1f}us  {px/tot/1e6:8.1f} Gpx/s  {gbs:7.0f} GB/s")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--all", action="store_true")
+    a = ap.parse_args()
+    print(torch.cuda.get_device_name(), "tile", ccl.tile_shape())
+    run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0))
+    if a.all:
+        for v in ["rc2fl", "cc2fl", "nc2fl"]:
+            run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0), v)
+        for d in (0.1, 0.3, 0.7, 0.9):
+            run(f"random 8192 d{d}", ccl.random_image(8192, 8192, d, 0))
+        for k in ("blobs", "spiral", "stripes", "checkerboard"):
+            run(f"{k} 8192", ccl.pattern_image(k, 8192, 8192))
+        run("random 2048 d0.5", ccl.random_image(2048, 2048, 0.5, 0))
+        run("random 512 d0.5", ccl.random_image(512, 512, 0.5, 0))
