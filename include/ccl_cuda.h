@@ -59,6 +59,8 @@ void* ccl_ctx_stream(ccl_ctx* ctx);
 
 /* Device-resident path (the timed roofline path).  d_img: H rows of
  * `img_pitch` bytes (pitch >= w).  d_labels: W*H u32, row-major, stride W.
+ * The context owns the kernel (a)->(e) work buffer (grown on first use), so
+ * calls sharing a context must be ordered on one stream.
  * Enqueued on `stream` exactly as given (NULL = the legacy default stream;
  * pass ccl_ctx_stream(ctx) for the context's own stream); asynchronous.
  * `timing` (may be NULL) is filled after the call only if `sync` != 0. */
@@ -96,16 +98,21 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
  * Steps 2-4 must all run before step 5; the strip's label buffer is not a
  * valid forest between 2 and 4. */
 ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
-                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream);
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, void* d_work, int variant,
+                           void* stream);
 ccl_status ccl_strip_seam_export(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
                                  uint32_t strip_index, uint32_t* d_labels, uint32_t* d_seam_out, void* stream);
 ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint32_t n_strips,
                                   uint32_t strip_index, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
                                   uint32_t* d_labels, uint32_t* d_scratch, void* stream);
-ccl_status ccl_strip_final(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
-                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream);
-/* d_scratch for ccl_strip_seam_resolve must hold ccl_strip_scratch_words(n_strips, w) u32. */
+ccl_status ccl_strip_final(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
+                           uint32_t* d_labels, const void* d_work, void* stream);
+/* d_scratch for ccl_strip_seam_resolve must hold ccl_strip_scratch_words(n_strips, w) u32;
+ * d_work (kernel (a) -> kernel (e) hand-off: per-tile masks, run table and
+ * seam-root list) must hold ccl_work_bytes(w, h, 1) bytes and stay untouched
+ * between ccl_strip_local and ccl_strip_final of the same strip. */
 size_t ccl_strip_scratch_words(uint32_t n_strips, uint32_t w);
+size_t ccl_work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
 
 /* GPU compaction (pipeline.cpp:54-70, "next" row (f)1): labels 1..K in raster
  * order of first appearance, background 0; K written to *k_out (host).

@@ -67,6 +67,8 @@ struct ccl_ctx {
     size_t h_img_bytes = 0;
     uint32_t* h_lab = nullptr;  // pinned
     size_t h_lab_bytes = 0;
+    void* d_work = nullptr;     // kernel (a) -> (e) hand-off buffer
+    size_t d_work_bytes = 0;
     ccl_timing last{};
 };
 
@@ -157,6 +159,16 @@ ccl_status read_timing(ccl_ctx* ctx, ccl_timing* t) {
     return CCL_OK;
 }
 
+ccl_status ensure_work(ccl_ctx* ctx, size_t bytes) {
+    if (ctx->d_work_bytes >= bytes) return CCL_OK;
+    if (ctx->d_work) cudaFree(ctx->d_work);
+    ctx->d_work = nullptr;
+    ctx->d_work_bytes = 0;
+    CCL_CHECK(cudaMalloc(&ctx->d_work, bytes));
+    ctx->d_work_bytes = bytes;
+    return CCL_OK;
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -206,6 +218,7 @@ void ccl_ctx_destroy(ccl_ctx* c) {
     if (c->d_lab) cudaFree(c->d_lab);
     if (c->h_img) cudaFreeHost(c->h_img);
     if (c->h_lab) cudaFreeHost(c->h_lab);
+    if (c->d_work) cudaFree(c->d_work);
     delete c;
 }
 
@@ -221,6 +234,8 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
     if (ccl_status s = make_geo(w, h, 0, img_pitch, img_pitch * h, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, 1))) return s;
+    a.work = static_cast<uint32_t*>(ctx->d_work);
     if (ccl_status s = run_pipeline(ctx, a, true)) return s;
     if (sync) return read_timing(ctx, timing);
     return CCL_OK;
@@ -238,6 +253,8 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ccl_status s = prepare(&a, d_frames, img_pitch, frame_pitch, n, d_labels, variant, st)) return s;
+    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, n))) return s;
+    a.work = static_cast<uint32_t*>(ctx->d_work);
     return run_pipeline(ctx, a, true);
 }
 
@@ -285,14 +302,16 @@ ccl_status strip_geo(uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, siz
 }  // namespace
 
 ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
-                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream) {
-    if (!ctx || !d_img || !d_labels) return fail(CCL_EINVAL, "null argument");
+                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, void* d_work, int variant,
+                           void* stream) {
+    if (!ctx || !d_img || !d_labels || !d_work) return fail(CCL_EINVAL, "null argument");
     if (img_pitch < w) return fail(CCL_EINVAL, "image pitch smaller than width");
     DeviceGuard dg(ctx->device);
     cclk::LaunchArgs a{};
     if (ccl_status s = strip_geo(w, h, row0, full_h, img_pitch, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    a.work = static_cast<uint32_t*>(d_work);
     CCL_CHECK(cclk::launch_local(a));
     CCL_CHECK(cclk::launch_seams(a));
     return CCL_OK;
@@ -323,20 +342,24 @@ ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint
     return CCL_OK;
 }
 
-ccl_status ccl_strip_final(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
-                           uint32_t row0, uint32_t full_h, uint32_t* d_labels, int variant, void* stream) {
-    if (!ctx || !d_img || !d_labels) return fail(CCL_EINVAL, "null argument");
-    if (img_pitch < w) return fail(CCL_EINVAL, "image pitch smaller than width");
+ccl_status ccl_strip_final(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, uint32_t* d_labels,
+                           const void* d_work, void* stream) {
+    if (!ctx || !d_labels || !d_work) return fail(CCL_EINVAL, "null argument");
     DeviceGuard dg(ctx->device);
     cclk::LaunchArgs a{};
-    if (ccl_status s = strip_geo(w, h, row0, full_h, img_pitch, &a.g)) return s;
+    if (ccl_status s = strip_geo(w, h, row0, full_h, w, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    // kernel (e) never reads the image; any 16B-aligned pointer satisfies prepare()
+    if (ccl_status s = prepare(&a, reinterpret_cast<const uint8_t*>(d_work), 16, 16 * size_t(h), 1, d_labels, 0, st))
+        return s;
+    a.work = static_cast<uint32_t*>(const_cast<void*>(d_work));
     CCL_CHECK(cclk::launch_final(a));
     return CCL_OK;
 }
 
 size_t ccl_strip_scratch_words(uint32_t n_strips, uint32_t w) { return size_t(n_strips) * 2 * w; }
+
+size_t ccl_work_bytes(uint32_t w, uint32_t h, uint32_t nframes) { return cclk::work_bytes(w, h, nframes); }
 
 // ---------------------------------------------------------------- compaction
 ccl_status ccl_compact_device(ccl_ctx* ctx, const uint32_t* d_raw, uint32_t w, uint32_t h, uint32_t* d_out,

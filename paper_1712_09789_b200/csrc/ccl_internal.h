@@ -38,6 +38,7 @@ struct LaunchArgs {
     CUtensorMap tm_lab;     // u32 {W, H, F}, box {32, 32, 1}, 128B swizzle
     const uint8_t* img;
     uint32_t* labels;
+    uint32_t* work;         // per-tile masks / run table / seam-root list (work_bytes)
     cudaStream_t stream;
 };
 
@@ -53,6 +54,7 @@ cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* seam_all, uint32_
 cudaError_t launch_compact(const uint32_t* raw, size_t n, uint32_t* out, uint32_t* scratch, cudaStream_t s);
 size_t compact_scratch_words(size_t n);
 
+size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
 int tile_w();
 int tile_h();
 

@@ -1,17 +1,21 @@
-// ccl_kernels.cu — the five hand-written sm_100a kernels of the labeler.
+// ccl_kernels.cu — the hand-written sm_100a kernels of the labeler.
 //
 //   (a)+(b)+(c)  k_local  : TMA-stage a TW x TH tile, warp-bit run detection
 //                           (coarse row scan), coarse column link, smem
-//                           min-union refinement, flatten (unification);
-//                           exports only the tile's seam labels + registers
-//                           the seam-touching local roots in the label buffer.
+//                           min-union refinement, flatten (unification).
+//                           Exports, per tile, a compact RUN TABLE (one u16
+//                           local root per row run), the row-word masks and
+//                           the list of seam-touching roots; writes the tile's
+//                           seam pixels and registers the seam-touching roots
+//                           as nodes of the global forest in the label buffer.
 //   (d)          k_seams  : boundary-only pass (Algorithm 2): one thread per
 //                           interior tile-seam pixel pair, global atomicMin
 //                           union-find directly in the label buffer.
-//   (e)          k_final  : recomputes the tile's local labels (cheaper than a
-//                           4 B/px round trip), resolves seam-touching roots
-//                           through the global forest, and writes every
-//                           label exactly once with swizzled TMA stores.
+//   (e)          k_final  : resolves each seam-touching root ONCE through the
+//                           global forest, expands the run table to pixels and
+//                           writes every label exactly once (swizzled TMA
+//                           stores).  It never re-reads the image: masks
+//                           (0.125 B/px) + run table (~0.5 B/px at d=0.5).
 //
 // The reference's block config / variant are honoured for validation and
 // strategy selection; the GPU tile is an internal constant (labels are
@@ -36,10 +40,25 @@ struct Cfg {
     static constexpr int F_OFF = P_BYTES;
     static constexpr int M_OFF = F_OFF + ((FW * 4 + 127) / 128) * 128;
     static constexpr int IMG_OFF = M_OFF + ((TH * WX * 4 + 127) / 128) * 128;
-    static constexpr int BAR_OFF = IMG_OFF + TW * TH;
+    static constexpr int PRE_OFF = IMG_OFF + TW * TH;
+    static constexpr int BAR_OFF = PRE_OFF + ((FW * 2 + 127) / 128) * 128;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
-    static_assert(NWARP * 4096 <= NODES * 4, "output staging must fit in the node array");
+    // work buffer (global) per tile
+    static constexpr int MASK_WORDS = TH * WX;                    // row-word masks
+    static constexpr int MAXF = TW + 2 * TH;                      // bound on seam-touching roots
+    static constexpr int HDR_WORDS = ((1 + NWARP + MAXF) + 3) / 4 * 4;  // nF, run count per warp, F list
+    static constexpr int TBL_PER_WARP = 512;                      // u16 run entries (<= 16 runs x 32 rows)
+    // kernel (e) smem
+    static constexpr int E_M_OFF = 0;
+    static constexpr int E_HDR_OFF = E_M_OFF + MASK_WORDS * 4;
+    static constexpr int E_FT_OFF = E_HDR_OFF + HDR_WORDS * 4;
+    static constexpr int E_TBL_OFF = E_FT_OFF + MAXF * 4;
+    static constexpr int E_STG_OFF = ((E_TBL_OFF + NWARP * TBL_PER_WARP * 2) + 1023) / 1024 * 1024;
+    static constexpr int E_BAR_OFF = E_STG_OFF + NWARP * 4096;
+    static constexpr int E_SMEM = E_BAR_OFF + 64 + 1024;
     static_assert(TW <= 256 && TH <= 256, "TMA box dims are limited to 256");
+    static_assert(NWARP * TBL_PER_WARP * 2 <= TW * TH, "run-table staging must fit in the image area");
+    static_assert(NODES < 0x8000, "node ids must leave bit 15 free for the seam-root tag");
 };
 
 using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
@@ -47,6 +66,32 @@ using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ uint8_t smem_raw[];
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+}
+
+// Work-buffer views of one tile (tile index tg over frames x tile rows x tile cols).
+template <class C>
+struct Work {
+    uint32_t* masks;
+    uint32_t* hdr;
+    uint16_t* tbl;
+    __device__ __forceinline__ Work(uint32_t* work, size_t ntiles, size_t tg) {
+        masks = work + tg * C::MASK_WORDS;
+        hdr = work + ntiles * C::MASK_WORDS + tg * C::HDR_WORDS;
+        tbl = reinterpret_cast<uint16_t*>(work + ntiles * (C::MASK_WORDS + C::HDR_WORDS)) +
+              tg * size_t(C::NWARP * C::TBL_PER_WARP);
+    }
+};
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // Per-lane result of the tile-local phase.
@@ -233,31 +278,85 @@ __device__ __forceinline__ uint32_t node_gidx(uint32_t node, uint32_t x0, uint32
 // ------------------------------------------------------------------ kernel (a)(b)(c)
 template <class C, int VAR, bool TMA>
 __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img,
-                                                 uint32_t* L, Geo g) {
+                                                    uint32_t* L, uint32_t* work, Geo g) {
     uint8_t* smem = aligned_smem();
     const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
     if (TMA && threadIdx.x == 0) prefetch_tmap(&tm_img);
     const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
     const uint32_t* P = reinterpret_cast<const uint32_t*>(smem);
     const uint32_t* F = reinterpret_cast<const uint32_t*>(smem + C::F_OFF);
+    const uint32_t* M = reinterpret_cast<const uint32_t*>(smem + C::M_OFF);
+    uint16_t* PRE = reinterpret_cast<uint16_t*>(smem + C::PRE_OFF);
+    uint16_t* STG = reinterpret_cast<uint16_t*>(smem + C::IMG_OFF);  // image tile is dead: run-table staging
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane, col0 = wx * 32;
     const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
     const uint32_t nbase = uint32_t(row * C::PS + col0);
     uint32_t* Lf = L + size_t(fz) * g.frame_px;  // strip/frame-local index = global - base
+    const size_t ntiles = size_t(g.ntx) * g.nty * gridDim.z;
+    const Work<C> wk(work, ntiles, (size_t(fz) * g.nty + ty) * g.ntx + tx);
 
-    // register seam-touching roots as global forest nodes: L[g] = g
-    uint32_t t = s.rootmask;
-    while (t) {
-        const uint32_t b = __ffs(t) - 1;
-        t &= t - 1;
-        const uint32_t n = nbase + b;
-        if ((F[n >> 5] >> (n & 31)) & 1u) {
-            const uint32_t gi = node_gidx<C>(n, x0, y0, g);
+    // ranks of the seam-touching roots (prefix popcount over the F bitmap)
+    if (warp == 0) {
+        uint32_t carry = 0;
+        for (int b0 = 0; b0 < C::FW; b0 += 32) {
+            const int i = b0 + lane;
+            const uint32_t c = i < C::FW ? __popc(F[i]) : 0u;
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (i < C::FW) PRE[i] = uint16_t(carry + inc - c);
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) wk.hdr[0] = carry;
+    }
+    // run table: one u16 per row run, in (row, run) order per warp; seam-touching
+    // roots are tagged 0x8000 | rank (the index into this tile's seam-root list)
+    const uint32_t rst = s.m & ~(s.m << 1);
+    const uint32_t cnt = __popc(rst);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    __syncthreads();  // PRE ready
+    {
+        uint16_t* dst = STG + warp * C::TBL_PER_WARP + (inc - cnt);
+        uint32_t t = rst;
+        while (t) {
+            const uint32_t b = __ffs(t) - 1;
+            t &= t - 1;
+            const uint32_t r = P[nbase + b];
+            const uint32_t fw = F[r >> 5], bit = 1u << (r & 31);
+            *dst++ = (fw & bit) ? uint16_t(0x8000u | (PRE[r >> 5] + __popc(fw & (bit - 1u)))) : uint16_t(r);
+        }
+    }
+    if (lane == 0) wk.hdr[1 + warp] = total;
+    // seam-root list (global raster indices, rank order) + forest registration L[g] = g
+    for (int i = tid; i < C::FW; i += C::NT) {
+        uint32_t bits = F[i];
+        uint32_t k = PRE[i];
+        while (bits) {
+            const uint32_t b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint32_t gi = node_gidx<C>(uint32_t(i) * 32 + b, x0, y0, g);
+            wk.hdr[1 + C::NWARP + k++] = gi;
             Lf[gi - g.base] = gi;
         }
     }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && total) bulk_store(wk.tbl + warp * C::TBL_PER_WARP, STG + warp * C::TBL_PER_WARP, (total * 2 + 15) & ~15u);
+    __syncthreads();
+    if (tid == 0) bulk_store(wk.masks, M, C::MASK_WORDS * 4);
+    if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+
     // seam pixels: their local root (global index) or background
     const bool has_top = ty > 0 || g.edge_above;
     const bool has_bot = ty + 1 < g.nty || g.edge_below;
@@ -289,6 +388,7 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
             Lf[size_t(gy) * g.W + x0 + C::TW - 1] = v;
         }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ kernel (d)
@@ -332,125 +432,145 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* L, Geo g) {
 }
 
 // ------------------------------------------------------------------ kernel (e)
-template <class C, int VAR, bool TMA, bool TMA_ST>
-__global__ void __launch_bounds__(C::NT, 3) k_final(const __grid_constant__ CUtensorMap tm_img,
-                                                 const __grid_constant__ CUtensorMap tm_lab, const uint8_t* img,
-                                                 uint32_t* L, Geo g) {
+// Reads only the tile's masks + run table + seam-root list (written by (a)),
+// resolves each seam-touching root once through the global forest, expands
+// runs to pixels and writes every label exactly once.
+template <class C, bool TMA_ST>
+__global__ void __launch_bounds__(C::NT, 4) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+                                                    const uint32_t* work, Geo g) {
     uint8_t* smem = aligned_smem();
+    uint32_t* M = reinterpret_cast<uint32_t*>(smem + C::E_M_OFF);
+    uint32_t* HDR = reinterpret_cast<uint32_t*>(smem + C::E_HDR_OFF);
+    uint32_t* FT = reinterpret_cast<uint32_t*>(smem + C::E_FT_OFF);
+    uint16_t* TBL = reinterpret_cast<uint16_t*>(smem + C::E_TBL_OFF);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::E_BAR_OFF);
     const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
-    if (threadIdx.x == 0) {
-        if (TMA) prefetch_tmap(&tm_img);
-        if (TMA_ST) prefetch_tmap(&tm_lab);
-    }
-    const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
-    uint32_t* P = reinterpret_cast<uint32_t*>(smem);
-    const uint32_t* F = reinterpret_cast<const uint32_t*>(smem + C::F_OFF);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
-    const int row = wy * 32 + lane, col0 = wx * 32;
+    const int row = wy * 32 + lane;
     const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
-    const uint32_t nbase = uint32_t(row * C::PS + col0);
     uint32_t* Lf = L + size_t(fz) * g.frame_px;
+    const size_t ntiles = size_t(g.ntx) * g.nty * gridDim.z;
+    const Work<C> wk(const_cast<uint32_t*>(work), ntiles, (size_t(fz) * g.nty + ty) * g.ntx + tx);
 
-    // (e1) final label of each local root; seam-touching roots walk the global forest
+    if (tid == 0) {
+        if (TMA_ST) prefetch_tmap(&tm_lab);
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, (C::MASK_WORDS + C::HDR_WORDS) * 4);
+        bulk_load(M, wk.masks, C::MASK_WORDS * 4, bar);
+        bulk_load(HDR, wk.hdr, C::HDR_WORDS * 4, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    const uint32_t m = M[row * C::WX + wx];
+    const uint32_t st = m & ~(m << 1);
+    const uint32_t cnt = __popc(st);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    {   // this warp's run entries -> smem (coalesced 16-byte loads)
+        const uint4* src = reinterpret_cast<const uint4*>(wk.tbl + warp * C::TBL_PER_WARP);
+        uint4* dst = reinterpret_cast<uint4*>(TBL + warp * C::TBL_PER_WARP);
+        for (uint32_t i = lane; i < (total * 2 + 15) / 16; i += 32) dst[i] = __ldg(src + i);
+    }
+    // each seam-touching root resolved once through the global forest
+    const uint32_t nF = HDR[0];
+    for (uint32_t k = tid; k < nF; k += C::NT) FT[k] = gfind_ro(Lf, g.base, HDR[1 + C::NWARP + k]);
+    __syncthreads();
+
+    // run labels at the run starts of this lane's staging row, then expand
+    uint8_t* stg = smem + C::E_STG_OFF + warp * 4096;  // 32 x 32 u32, 128B-swizzled
+    uint8_t* myrow = stg + lane * 128;
+    const int sw = lane & 7;
     {
-        uint32_t t = s.rootmask;
+        const uint16_t* e = TBL + warp * C::TBL_PER_WARP + (inc - cnt);
+        uint32_t t = st;
         while (t) {
             const uint32_t b = __ffs(t) - 1;
             t &= t - 1;
-            const uint32_t n = nbase + b;
-            const uint32_t gi = node_gidx<C>(n, x0, y0, g);
-            P[n] = ((F[n >> 5] >> (n & 31)) & 1u) ? gfind_ro(Lf, g.base, gi) : gi;
+            const uint32_t v = *e++;
+            const uint32_t lab = (v & 0x8000u) ? FT[v & 0x7FFFu] : node_gidx<C>(v, x0, y0, g);
+            *reinterpret_cast<uint32_t*>(myrow + ((((b >> 2) ^ sw) << 4) | ((b & 3) << 2))) = lab;
         }
     }
-    __syncthreads();
-    // (e2) expand to pixels: root segments hold the label, others point at their root
-    uint32_t lab[32];
     uint32_t cur = kBG;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        if ((s.st >> i) & 1u) {
-            const uint32_t v = P[nbase + i];
-            if ((s.rootmask >> i) & 1u) cur = v;
-            else cur = P[v];
-        }
-        lab[i] = ((s.m >> i) & 1u) ? cur : kBG;
-    }
-    __syncthreads();  // node array is dead from here on: reuse it as the store staging
-    if (TMA_ST) {
-        uint8_t* stg = smem + warp * 4096;  // 32x32 u32, 128B-swizzled (1024B-aligned)
+    for (int c = 0; c < 8; ++c) {
+        uint4* p = reinterpret_cast<uint4*>(myrow + ((c ^ sw) << 4));
+        uint4 v = *p;
+        uint32_t a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const uint4 v = make_uint4(lab[4 * c], lab[4 * c + 1], lab[4 * c + 2], lab[4 * c + 3]);
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = v;
+        for (int q = 0; q < 4; ++q) {
+            const int i = 4 * c + q;
+            cur = ((st >> i) & 1u) ? a[q] : cur;
+            a[q] = ((m >> i) & 1u) ? cur : kBG;
         }
+        if (TMA_ST) {
+            *p = make_uint4(a[0], a[1], a[2], a[3]);
+        } else {
+            const uint32_t gy = y0 + row;
+            if (gy < g.H) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t gx = x0 + wx * 32 + 4 * c + q;
+                    if (gx < g.W) Lf[size_t(gy) * g.W + gx] = a[q];
+                }
+            }
+        }
+    }
+    if (TMA_ST) {
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            tma_store_3d(&tm_lab, int(x0 + col0), int(y0 + wy * 32), int(fz), stg);  // OOB clipped
+            tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(fz), stg);  // OOB clipped
             tma_store_commit_and_wait();
-        }
-    } else {
-        const uint32_t gy = y0 + row;
-        if (gy < g.H) {
-            uint32_t* dst = Lf + size_t(gy) * g.W;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t gx = x0 + col0 + i;
-                if (gx < g.W) dst[gx] = lab[i];
-            }
         }
     }
 }
 
 // ================================================================== host side
 template <int VAR>
-static cudaError_t launch_variant(const LaunchArgs& a, int phase) {
+static cudaError_t launch_local_v(const LaunchArgs& a) {
     using C = TileCfg;
     const dim3 grid(a.g.ntx, a.g.nty, a.nframes);
-    const dim3 block(C::NT);
-    if (phase == 0) {
-        if (a.tma_load) {
-            auto k = k_local<C, VAR, true>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-            k<<<grid, block, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.g);
-        } else {
-            auto k = k_local<C, VAR, false>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-            k<<<grid, block, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.g);
-        }
+    if (a.tma_load) {
+        auto k = k_local<C, VAR, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        k<<<grid, C::NT, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.work, a.g);
     } else {
-#define CCL_LAUNCH_FINAL(TL, TS)                                                             \
-    {                                                                                        \
-        auto k = k_final<C, VAR, TL, TS>;                                                    \
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);       \
-        k<<<grid, block, C::SMEM, a.stream>>>(a.tm_img, a.tm_lab, a.img, a.labels, a.g);     \
-    }
-        if (a.tma_load && a.tma_store) CCL_LAUNCH_FINAL(true, true)
-        else if (a.tma_load) CCL_LAUNCH_FINAL(true, false)
-        else if (a.tma_store) CCL_LAUNCH_FINAL(false, true)
-        else CCL_LAUNCH_FINAL(false, false)
-#undef CCL_LAUNCH_FINAL
+        auto k = k_local<C, VAR, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        k<<<grid, C::NT, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.work, a.g);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_local(const LaunchArgs& a) {
     switch (a.variant) {
-        case 0: return launch_variant<0>(a, 0);
-        case 1: return launch_variant<1>(a, 0);
-        case 2: return launch_variant<2>(a, 0);
-        default: return launch_variant<3>(a, 0);
+        case 0: return launch_local_v<0>(a);
+        case 1: return launch_local_v<1>(a);
+        case 2: return launch_local_v<2>(a);
+        default: return launch_local_v<3>(a);
     }
 }
 
 cudaError_t launch_final(const LaunchArgs& a) {
-    switch (a.variant) {
-        case 0: return launch_variant<0>(a, 1);
-        case 1: return launch_variant<1>(a, 1);
-        case 2: return launch_variant<2>(a, 1);
-        default: return launch_variant<3>(a, 1);
+    using C = TileCfg;
+    const dim3 grid(a.g.ntx, a.g.nty, a.nframes);
+    if (a.tma_store) {
+        auto k = k_final<C, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::E_SMEM);
+        k<<<grid, C::NT, C::E_SMEM, a.stream>>>(a.tm_lab, a.labels, a.work, a.g);
+    } else {
+        auto k = k_final<C, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::E_SMEM);
+        k<<<grid, C::NT, C::E_SMEM, a.stream>>>(a.tm_lab, a.labels, a.work, a.g);
     }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_seams(const LaunchArgs& a) {
@@ -459,6 +579,12 @@ cudaError_t launch_seams(const LaunchArgs& a) {
     const dim3 grid(unsigned((n + 255) / 256), a.nframes);
     k_seams<TileCfg><<<grid, 256, 0, a.stream>>>(a.labels, a.g);
     return cudaGetLastError();
+}
+
+size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes) {
+    using C = TileCfg;
+    const size_t ntiles = size_t((w + C::TW - 1) / C::TW) * ((h + C::TH - 1) / C::TH) * nframes;
+    return ntiles * (size_t(C::MASK_WORDS + C::HDR_WORDS) * 4 + size_t(C::NWARP) * C::TBL_PER_WARP * 2);
 }
 
 int tile_w() { return TileCfg::TW; }

@@ -57,6 +57,7 @@ class StripLabeler:
         self.rank, self.world, self.group = rank, world, group
         self.seam = torch.empty(4 * w, dtype=torch.int32, device=device)
         self.scratch = torch.empty(int(_lib.ccl_strip_scratch_words(world, w)), dtype=torch.int32, device=device)
+        self.work = torch.empty(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=device)
 
     def label(self, img, out, variant="c2fl", stream=None):
         import torch
@@ -64,7 +65,7 @@ class StripLabeler:
         s = _stream_ptr(stream)
         c = self.ctx.handle
         _check(_lib.ccl_strip_local(c, img.data_ptr(), img.stride(0), self.w, self.h, self.row0, self.full_h,
-                                    out.data_ptr(), v, s))
+                                    out.data_ptr(), self.work.data_ptr(), v, s))
         _check(_lib.ccl_strip_seam_export(c, self.w, self.h, self.row0, self.full_h, self.rank, out.data_ptr(),
                                           self.seam.data_ptr(), s))
         if stream is not None:
@@ -74,8 +75,8 @@ class StripLabeler:
             allseams = exchange_seams(self.seam, self.world, self.group)
         _check(_lib.ccl_strip_seam_resolve(c, allseams.data_ptr(), self.world, self.rank, self.w, self.h, self.row0,
                                            self.full_h, out.data_ptr(), self.scratch.data_ptr(), s))
-        _check(_lib.ccl_strip_final(c, img.data_ptr(), img.stride(0), self.w, self.h, self.row0, self.full_h,
-                                    out.data_ptr(), v, s))
+        _check(_lib.ccl_strip_final(c, self.w, self.h, self.row0, self.full_h, out.data_ptr(), self.work.data_ptr(),
+                                    s))
         return out
 
 
@@ -97,12 +98,14 @@ def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx
     views = []
     for k, (r0, h) in enumerate(parts):
         im, lo = img[r0:r0 + h], out[r0:r0 + h]
-        views.append((im, lo, r0, h))
-        _check(_lib.ccl_strip_local(ctx.handle, im.data_ptr(), im.stride(0), w, h, r0, h_full, lo.data_ptr(), v, s))
+        wk = torch.empty(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=img.device)
+        views.append((im, lo, r0, h, wk))
+        _check(_lib.ccl_strip_local(ctx.handle, im.data_ptr(), im.stride(0), w, h, r0, h_full, lo.data_ptr(),
+                                    wk.data_ptr(), v, s))
         _check(_lib.ccl_strip_seam_export(ctx.handle, w, h, r0, h_full, k, lo.data_ptr(), seams[k].data_ptr(), s))
-    for k, (im, lo, r0, h) in enumerate(views):
+    for k, (im, lo, r0, h, wk) in enumerate(views):
         _check(_lib.ccl_strip_seam_resolve(ctx.handle, seams.data_ptr(), n_strips, k, w, h, r0, h_full, lo.data_ptr(),
                                            scratch.data_ptr(), s))
-    for k, (im, lo, r0, h) in enumerate(views):
-        _check(_lib.ccl_strip_final(ctx.handle, im.data_ptr(), im.stride(0), w, h, r0, h_full, lo.data_ptr(), v, s))
+    for k, (im, lo, r0, h, wk) in enumerate(views):
+        _check(_lib.ccl_strip_final(ctx.handle, w, h, r0, h_full, lo.data_ptr(), wk.data_ptr(), s))
     return out
