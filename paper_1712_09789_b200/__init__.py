@@ -35,7 +35,7 @@ __all__ = [
 
 BG = 0xFFFFFFFF
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_lib", "libccl_b200.so")
+_LIB_PATH = os.environ.get("CCL_LIB_PATH") or os.path.join(_HERE, "_lib", "libccl_b200.so")
 
 
 def lib_path() -> str:

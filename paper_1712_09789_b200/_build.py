@@ -19,6 +19,10 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libccl_b200.so")
+
+
+def lib_for_tile(tile: str | None) -> str:
+    return LIB if not tile else os.path.join(OUT_DIR, f"libccl_b200_{tile}.so")
 OBJ_DIR = os.path.join(REPO, "build", "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -79,14 +83,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(r.stdout + r.stderr, file=sys.stderr)
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed:\n" + " ".join(r.args) + "\n" + r.stdout + r.stderr)
-    if force or jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        tmp = LIB + ".tmp"
+    lib = lib_for_tile(os.environ.get("CCL_TILE"))
+    if force or jobs or not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        tmp = lib + ".tmp"
         link = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

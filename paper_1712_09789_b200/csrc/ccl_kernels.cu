@@ -40,8 +40,8 @@ struct Cfg {
     static constexpr int F_OFF = P_BYTES;
     static constexpr int M_OFF = F_OFF + ((FW * 4 + 127) / 128) * 128;
     static constexpr int IMG_OFF = M_OFF + ((TH * WX * 4 + 127) / 128) * 128;
-    static constexpr int PRE_OFF = IMG_OFF + TW * TH;
-    static constexpr int BAR_OFF = PRE_OFF + ((FW * 2 + 127) / 128) * 128;
+    static constexpr int FR_OFF = IMG_OFF + TW * TH;
+    static constexpr int BAR_OFF = FR_OFF + ((4 * (1 + TW + 2 * TH) + 127) / 128) * 128;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
     // work buffer (global) per tile
     static constexpr int MASK_WORDS = TH * WX;                    // row-word masks
@@ -128,6 +128,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
         }
     }
     for (int i = tid; i < C::FW; i += C::NT) F[i] = 0u;
+    if (tid == 0) *reinterpret_cast<uint32_t*>(smem + C::FR_OFF) = 0u;
     uint32_t m;
     if (TMA) {
         __syncthreads();  // mbarrier init visible before anyone polls it
@@ -217,54 +218,36 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     }
     __syncthreads();
 
-    // ---- unification: every node points at its root.  Two passes: path-halving
-    // stores of other lanes may still overwrite an entry this lane has already
-    // flattened (with a valid but non-root ancestor), so pass 1 compresses and
-    // pass 2, after a barrier, re-reads the now short chains without writing
-    // anything but the node's own entry.
-    uint32_t rootmask = 0u;
-    {
-        uint32_t t = st;
-        while (t) {
-            const uint32_t b = __ffs(t) - 1;
-            t &= t - 1;
-            const uint32_t n = nbase + b;
-            const uint32_t r = sfind(P, n);
-            P[n] = r;
-            if (r == n) rootmask |= 1u << b;
-        }
-    }
-    __syncthreads();
-    {
-        volatile uint32_t* vP = P;
-        uint32_t t = st & ~rootmask;
-        while (t) {
-            const uint32_t b = __ffs(t) - 1;
-            t &= t - 1;
-            const uint32_t n = nbase + b;
-            uint32_t r = vP[n];
-            for (uint32_t q = vP[r]; q != r; q = vP[r]) r = q;
-            vP[n] = r;
-        }
-    }
-    __syncthreads();
-
-    // ---- flag roots of components touching a side that faces a neighbour
+    // ---- seam-touching roots (components reaching a side that faces a
+    // neighbour tile/strip): marked once via the F bitmap, ranked by arrival
+    // and TAGGED in their own entry (0x80000000 | rank) after a barrier, so a
+    // single read-only walk per run later yields either an interior root or
+    // the rank of a seam root.  No whole-tile flatten pass is needed.
     const bool has_top = ty > 0 || g.edge_above;
     const bool has_bot = ty + 1 < g.nty || g.edge_below;
     const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
-    auto mark = [&](uint32_t r) { atomicOr(&F[r >> 5], 1u << (r & 31)); };
+    uint32_t* FR = reinterpret_cast<uint32_t*>(smem + C::FR_OFF);  // [0] = count, [1..] = roots
+    auto mark = [&](uint32_t n) {
+        uint32_t x = n;
+        for (uint32_t p = P[x]; p != x; p = P[x]) x = p;
+        const uint32_t bit = 1u << (x & 31);
+        if (!(atomicOr(&F[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
+    };
     if (wy == 0 && has_top) {
         const uint32_t s0 = __shfl_sync(0xffffffffu, st, 0);
-        if ((s0 >> lane) & 1u) mark(P[col0 + lane]);
+        if ((s0 >> lane) & 1u) mark(col0 + lane);
     }
     if (wy == C::WY - 1 && has_bot) {
         const uint32_t sl = __shfl_sync(0xffffffffu, st, 31);
-        if ((sl >> lane) & 1u) mark(P[(C::TH - 1) * C::PS + col0 + lane]);
+        if ((sl >> lane) & 1u) mark((C::TH - 1) * C::PS + col0 + lane);
     }
-    if (wx == 0 && has_left && (m & 1u)) mark(P[nbase]);
-    if (wx == C::WX - 1 && has_right && (m >> 31)) mark(P[nbase + hi_bit_le(st, 31)]);
+    if (wx == 0 && has_left && (m & 1u)) mark(nbase);
+    if (wx == C::WX - 1 && has_right && (m >> 31)) mark(nbase + hi_bit_le(st, 31));
     __syncthreads();
+    const uint32_t nf = FR[0];
+    for (uint32_t k = tid; k < nf; k += C::NT) P[FR[1 + k]] = 0x80000000u | k;
+    __syncthreads();
+    const uint32_t rootmask = 0u;
     return LaneState{m, st, rootmask};
 }
 
@@ -273,6 +256,18 @@ __device__ __forceinline__ uint32_t node_gidx(uint32_t node, uint32_t x0, uint32
     const uint32_t r = node / C::PS;
     const uint32_t c = node - r * C::PS;
     return (g.row0 + y0 + r) * g.W + x0 + c;  // global raster index (convert_ids)
+}
+
+// Read-only walk to a run's root after tagging: returns the root node id and
+// sets `tag` to 0x80000000|rank for seam-touching roots (0 otherwise).
+__device__ __forceinline__ uint32_t walk_root(const uint32_t* P, uint32_t x, uint32_t& tag) {
+    uint32_t p = P[x];
+    while (p != x && !(p >> 31)) {
+        x = p;
+        p = P[x];
+    }
+    tag = (p >> 31) ? p : 0u;
+    return x;
 }
 
 // ------------------------------------------------------------------ kernel (a)(b)(c)
@@ -284,9 +279,7 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
     if (TMA && threadIdx.x == 0) prefetch_tmap(&tm_img);
     const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
     const uint32_t* P = reinterpret_cast<const uint32_t*>(smem);
-    const uint32_t* F = reinterpret_cast<const uint32_t*>(smem + C::F_OFF);
     const uint32_t* M = reinterpret_cast<const uint32_t*>(smem + C::M_OFF);
-    uint16_t* PRE = reinterpret_cast<uint16_t*>(smem + C::PRE_OFF);
     uint16_t* STG = reinterpret_cast<uint16_t*>(smem + C::IMG_OFF);  // image tile is dead: run-table staging
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
@@ -297,25 +290,11 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
     const size_t ntiles = size_t(g.ntx) * g.nty * gridDim.z;
     const Work<C> wk(work, ntiles, (size_t(fz) * g.nty + ty) * g.ntx + tx);
 
-    // ranks of the seam-touching roots (prefix popcount over the F bitmap)
-    if (warp == 0) {
-        uint32_t carry = 0;
-        for (int b0 = 0; b0 < C::FW; b0 += 32) {
-            const int i = b0 + lane;
-            const uint32_t c = i < C::FW ? __popc(F[i]) : 0u;
-            uint32_t inc = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            if (i < C::FW) PRE[i] = uint16_t(carry + inc - c);
-            carry += __shfl_sync(0xffffffffu, inc, 31);
-        }
-        if (lane == 0) wk.hdr[0] = carry;
-    }
+    const uint32_t* FR = reinterpret_cast<const uint32_t*>(smem + C::FR_OFF);
+    const uint32_t nf = FR[0];
+    if (tid == 0) wk.hdr[0] = nf;
     // run table: one u16 per row run, in (row, run) order per warp; seam-touching
-    // roots are tagged 0x8000 | rank (the index into this tile's seam-root list)
+    // roots carry 0x8000 | rank (the index into this tile's seam-root list)
     const uint32_t rst = s.m & ~(s.m << 1);
     const uint32_t cnt = __popc(rst);
     uint32_t inc = cnt;
@@ -325,30 +304,23 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
         if (lane >= o) inc += y;
     }
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    __syncthreads();  // PRE ready
     {
         uint16_t* dst = STG + warp * C::TBL_PER_WARP + (inc - cnt);
         uint32_t t = rst;
         while (t) {
             const uint32_t b = __ffs(t) - 1;
             t &= t - 1;
-            const uint32_t r = P[nbase + b];
-            const uint32_t fw = F[r >> 5], bit = 1u << (r & 31);
-            *dst++ = (fw & bit) ? uint16_t(0x8000u | (PRE[r >> 5] + __popc(fw & (bit - 1u)))) : uint16_t(r);
+            uint32_t tag;
+            const uint32_t r = walk_root(P, nbase + b, tag);
+            *dst++ = tag ? uint16_t(0x8000u | (tag & 0x7FFFu)) : uint16_t(r);
         }
     }
     if (lane == 0) wk.hdr[1 + warp] = total;
     // seam-root list (global raster indices, rank order) + forest registration L[g] = g
-    for (int i = tid; i < C::FW; i += C::NT) {
-        uint32_t bits = F[i];
-        uint32_t k = PRE[i];
-        while (bits) {
-            const uint32_t b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const uint32_t gi = node_gidx<C>(uint32_t(i) * 32 + b, x0, y0, g);
-            wk.hdr[1 + C::NWARP + k++] = gi;
-            Lf[gi - g.base] = gi;
-        }
+    for (uint32_t k = tid; k < nf; k += C::NT) {
+        const uint32_t gi = node_gidx<C>(FR[1 + k], x0, y0, g);
+        wk.hdr[1 + C::NWARP + k] = gi;
+        Lf[gi - g.base] = gi;
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -365,7 +337,7 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
         const uint32_t m0 = __shfl_sync(0xffffffffu, s.m, 0), s0 = __shfl_sync(0xffffffffu, s.st, 0);
         if (gx < g.W) {
             uint32_t v = kBG;
-            if ((m0 >> lane) & 1u) v = node_gidx<C>(P[col0 + hi_bit_le(s0, lane)], x0, y0, g);
+            if ((m0 >> lane) & 1u) { uint32_t tg; v = node_gidx<C>(walk_root(P, col0 + hi_bit_le(s0, lane), tg), x0, y0, g); }
             Lf[size_t(y0) * g.W + gx] = v;
         }
     }
@@ -373,18 +345,18 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
         const uint32_t ml = __shfl_sync(0xffffffffu, s.m, 31), sl = __shfl_sync(0xffffffffu, s.st, 31);
         if (gx < g.W) {
             uint32_t v = kBG;
-            if ((ml >> lane) & 1u) v = node_gidx<C>(P[(C::TH - 1) * C::PS + col0 + hi_bit_le(sl, lane)], x0, y0, g);
+            if ((ml >> lane) & 1u) { uint32_t tg; v = node_gidx<C>(walk_root(P, (C::TH - 1) * C::PS + col0 + hi_bit_le(sl, lane), tg), x0, y0, g); }
             Lf[size_t(y0 + C::TH - 1) * g.W + gx] = v;
         }
     }
     const uint32_t gy = y0 + row;
     if (gy < g.H) {
         if (wx == 0 && tx > 0) {
-            const uint32_t v = (s.m & 1u) ? node_gidx<C>(P[nbase], x0, y0, g) : kBG;
+            uint32_t tg; const uint32_t v = (s.m & 1u) ? node_gidx<C>(walk_root(P, nbase, tg), x0, y0, g) : kBG;
             Lf[size_t(gy) * g.W + x0] = v;
         }
         if (wx == C::WX - 1 && tx + 1 < g.ntx) {
-            const uint32_t v = (s.m >> 31) ? node_gidx<C>(P[nbase + hi_bit_le(s.st, 31)], x0, y0, g) : kBG;
+            uint32_t tg; const uint32_t v = (s.m >> 31) ? node_gidx<C>(walk_root(P, nbase + hi_bit_le(s.st, 31), tg), x0, y0, g) : kBG;
             Lf[size_t(gy) * g.W + x0 + C::TW - 1] = v;
         }
     }

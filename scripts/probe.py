@@ -38,9 +38,13 @@ def run(name, img_np, variant="c2fl", iters=10):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--all", action="store_true")
+    ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     print(torch.cuda.get_device_name(), "tile", ccl.tile_shape())
     run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0))
+    if a.quick:
+        run("spiral 8192", ccl.pattern_image("spiral", 8192, 8192))
+        run("random 8192 d0.7", ccl.random_image(8192, 8192, 0.7, 0))
     if a.all:
         for v in ["rc2fl", "cc2fl", "nc2fl"]:
             run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0), v)
