@@ -228,8 +228,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
     uint32_t* FR = reinterpret_cast<uint32_t*>(smem + C::FR_OFF);  // [0] = count, [1..] = roots
     auto mark = [&](uint32_t n) {
-        uint32_t x = n;
-        for (uint32_t p = P[x]; p != x; p = P[x]) x = p;
+        const uint32_t x = sfind(P, n);
         const uint32_t bit = 1u << (x & 31);
         if (!(atomicOr(&F[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
     };
@@ -260,6 +259,8 @@ __device__ __forceinline__ uint32_t node_gidx(uint32_t node, uint32_t x0, uint32
 
 // Read-only walk to a run's root after tagging: returns the root node id and
 // sets `tag` to 0x80000000|rank for seam-touching roots (0 otherwise).
+// (Path halving here was measured: it shortens spiral chains but costs more
+// than it saves on random d=0.5 tiles, whose chains are short.)
 __device__ __forceinline__ uint32_t walk_root(const uint32_t* P, uint32_t x, uint32_t& tag) {
     uint32_t p = P[x];
     while (p != x && !(p >> 31)) {
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
     const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
     if (TMA && threadIdx.x == 0) prefetch_tmap(&tm_img);
     const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
-    const uint32_t* P = reinterpret_cast<const uint32_t*>(smem);
+    uint32_t* P = reinterpret_cast<uint32_t*>(smem);
     const uint32_t* M = reinterpret_cast<const uint32_t*>(smem + C::M_OFF);
     uint16_t* STG = reinterpret_cast<uint16_t*>(smem + C::IMG_OFF);  // image tile is dead: run-table staging
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
