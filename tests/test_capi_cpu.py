@@ -106,4 +106,4 @@ def test_strip_split(ccl):
 
 def test_tile_shape(ccl):
     tw, th = ccl.tile_shape()
-    assert tw % 32 == 0 and th % 32 == 0 and tw <= 256 and th <= 256
+    assert tw % 32 == 0 and th % 32 == 0 and th <= 256
