@@ -164,17 +164,38 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     const uint32_t ust = RUNS ? (um & ~(um << 1)) : um;
     const uint32_t nbase = uint32_t(row * C::PS + col0);
 
-    // ---- init + coarse column scan (no atomics: plain parent links to the row above)
+    // ---- init + coarse column scan (no atomics: plain parent links upward).
+    // C2FL links a run to the first run above it that it overlaps -- and, since
+    // the masks of the rows above are at hand (shuffles), keeps climbing that
+    // first-overlap path up to CLIMB rows in registers, linking straight to the
+    // highest ancestor reached: vertical coarse chains come out CLIMB x shorter.
     {
+        constexpr int CLIMB = 4;
+        uint32_t ups[CLIMB];
+        ups[0] = um;
+#pragma unroll
+        for (int k = 1; k < CLIMB; ++k) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, m, k + 1);
+            ups[k] = lane > k ? v : 0u;  // rows above this warp's band are not climbed
+        }
         uint32_t t = st;
         while (t) {
             const uint32_t b = __ffs(t) - 1;
             t &= t - 1;
             uint32_t par = nbase + b;
-            if (VAR == 0) {  // C2FL: run -> upper run under its first overlap
+            if (VAR == 0) {  // C2FL: run -> ancestor along its first-overlap path
                 const uint32_t mb = m >> b;
-                const uint32_t ov = ((mb & ~(mb + 1u)) << b) & um;
-                if (ov) par = nbase - C::PS + hi_bit_le(ust, __ffs(ov) - 1);
+                uint32_t run = (mb & ~(mb + 1u)) << b;
+#pragma unroll
+                for (int k = 0; k < CLIMB; ++k) {
+                    const uint32_t ov = run & ups[k];
+                    if (!ov) break;
+                    const uint32_t u = ups[k];
+                    const uint32_t s = hi_bit_le(u & ~(u << 1), __ffs(ov) - 1);
+                    par = nbase - uint32_t(k + 1) * C::PS + s;
+                    const uint32_t ub = u >> s;
+                    run = (ub & ~(ub + 1u)) << s;
+                }
             } else if (VAR == 2) {  // CC2FL: pixel -> pixel above
                 if ((um >> b) & 1u) par = nbase + b - C::PS;
             }
