@@ -36,7 +36,7 @@ struct Cfg {
     static constexpr int PS = TW + 1;  // padded node row stride: node id order == raster order
     static constexpr int NODES = TH * PS;
     static constexpr int FW = (NODES + 31) / 32;
-    static constexpr int P_BYTES = ((NODES * 4 + 1023) / 1024) * 1024;
+    static constexpr int P_BYTES = ((NODES * 2 + 1023) / 1024) * 1024;  // u16 parents
     static constexpr int F_OFF = P_BYTES;
     static constexpr int M_OFF = F_OFF + ((FW * 4 + 127) / 128) * 128;
     static constexpr int IMG_OFF = M_OFF + ((TH * WX * 4 + 127) / 128) * 128;
@@ -62,6 +62,35 @@ struct Cfg {
 };
 
 using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
+
+// Node parents are u16 (node ids < 2^15; bit 15 tags seam roots): half the
+// shared memory of u32 parents -> more resident CTAs for this latency-bound
+// phase.  Unions are CAS min-unions on the 16-bit entries.
+using node_t = uint16_t;
+constexpr uint32_t kTag = 0x8000u;
+__device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
+    volatile node_t* vP = P;
+    uint32_t p = vP[x];
+    while (p != x) {
+        const uint32_t gp = vP[p];
+        if (gp == p) return p;
+        vP[x] = node_t(gp);  // path halving (ancestor only)
+        x = gp;
+        p = vP[x];
+    }
+    return x;
+}
+__device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = nfind(P, a);
+        b = nfind(P, b);
+        if (a == b) return;
+        if (a < b) { const uint32_t t = a; a = b; b = t; }
+        if (atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(a),
+                      static_cast<unsigned short>(b)) == a)
+            return;
+    }
+}
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ uint8_t smem_raw[];
@@ -108,7 +137,7 @@ struct LaneState {
 template <class C, int VAR, bool TMA>
 __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uint8_t* img, const Geo& g,
                                                 uint32_t tx, uint32_t ty, uint32_t fz, uint8_t* smem) {
-    uint32_t* P = reinterpret_cast<uint32_t*>(smem);
+    node_t* P = reinterpret_cast<node_t*>(smem);
     uint32_t* F = reinterpret_cast<uint32_t*>(smem + C::F_OFF);
     uint32_t* M = reinterpret_cast<uint32_t*>(smem + C::M_OFF);
     uint8_t* IMG = smem + C::IMG_OFF;
@@ -199,7 +228,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
             } else if (VAR == 2) {  // CC2FL: pixel -> pixel above
                 if ((um >> b) & 1u) par = nbase + b - C::PS;
             }
-            P[nbase + b] = par;
+            P[nbase + b] = node_t(par);
         }
     }
     __syncthreads();
@@ -212,7 +241,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
         while (U) {
             const uint32_t b = __ffs(U) - 1;
             U &= U - 1;
-            sunion(P, nbase + hi_bit_le(st, b), nbase - C::PS + hi_bit_le(ust, b));
+            nunion(P, nbase + hi_bit_le(st, b), nbase - C::PS + hi_bit_le(ust, b));
         }
     } else {
         if (VAR == 3) {  // NC2FL: every vertical pair
@@ -220,28 +249,28 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
             while (U) {
                 const uint32_t b = __ffs(U) - 1;
                 U &= U - 1;
-                sunion(P, nbase + b, nbase + b - C::PS);
+                nunion(P, nbase + b, nbase + b - C::PS);
             }
         }
         uint32_t hp = (m & (m << 1)) & ~(um & (um << 1));  // row pairs, minus closed 2x2 squares
         while (hp) {
             const uint32_t b = __ffs(hp) - 1;
             hp &= hp - 1;
-            sunion(P, nbase + b, nbase + b - 1);
+            nunion(P, nbase + b, nbase + b - 1);
         }
     }
     if (wx > 0 && (m & 1u)) {  // run continuing across the word boundary
         const uint32_t lm = M[row * C::WX + wx - 1];
         if (lm >> 31) {
             const uint32_t lst = RUNS ? (lm & ~(lm << 1)) : lm;
-            sunion(P, nbase, nbase - 32 + (31 - __clz(lst)));
+            nunion(P, nbase, nbase - 32 + (31 - __clz(lst)));
         }
     }
     __syncthreads();
 
     // ---- seam-touching roots (components reaching a side that faces a
     // neighbour tile/strip): marked once via the F bitmap, ranked by arrival
-    // and TAGGED in their own entry (0x80000000 | rank) after a barrier, so a
+    // and TAGGED in their own entry (0x8000 | rank) after a barrier, so a
     // single read-only walk per run later yields either an interior root or
     // the rank of a seam root.  No whole-tile flatten pass is needed.
     const bool has_top = ty > 0 || g.edge_above;
@@ -249,7 +278,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
     uint32_t* FR = reinterpret_cast<uint32_t*>(smem + C::FR_OFF);  // [0] = count, [1..] = roots
     auto mark = [&](uint32_t n) {
-        const uint32_t x = sfind(P, n);
+        const uint32_t x = nfind(P, n);
         const uint32_t bit = 1u << (x & 31);
         if (!(atomicOr(&F[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
     };
@@ -265,7 +294,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     if (wx == C::WX - 1 && has_right && (m >> 31)) mark(nbase + hi_bit_le(st, 31));
     __syncthreads();
     const uint32_t nf = FR[0];
-    for (uint32_t k = tid; k < nf; k += C::NT) P[FR[1 + k]] = 0x80000000u | k;
+    for (uint32_t k = tid; k < nf; k += C::NT) P[FR[1 + k]] = node_t(kTag | k);
     __syncthreads();
     const uint32_t rootmask = 0u;
     return LaneState{m, st, rootmask};
@@ -279,16 +308,16 @@ __device__ __forceinline__ uint32_t node_gidx(uint32_t node, uint32_t x0, uint32
 }
 
 // Read-only walk to a run's root after tagging: returns the root node id and
-// sets `tag` to 0x80000000|rank for seam-touching roots (0 otherwise).
+// sets `tag` to 0x8000|rank for seam-touching roots (0 otherwise).
 // (Path halving here was measured: it shortens spiral chains but costs more
 // than it saves on random d=0.5 tiles, whose chains are short.)
-__device__ __forceinline__ uint32_t walk_root(const uint32_t* P, uint32_t x, uint32_t& tag) {
+__device__ __forceinline__ uint32_t walk_root(const node_t* P, uint32_t x, uint32_t& tag) {
     uint32_t p = P[x];
-    while (p != x && !(p >> 31)) {
+    while (p != x && !(p & kTag)) {
         x = p;
         p = P[x];
     }
-    tag = (p >> 31) ? p : 0u;
+    tag = (p & kTag) ? p : 0u;
     return x;
 }
 
@@ -300,7 +329,7 @@ __global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUte
     const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
     if (TMA && threadIdx.x == 0) prefetch_tmap(&tm_img);
     const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
-    uint32_t* P = reinterpret_cast<uint32_t*>(smem);
+    node_t* P = reinterpret_cast<node_t*>(smem);
     const uint32_t* M = reinterpret_cast<const uint32_t*>(smem + C::M_OFF);
     uint16_t* STG = reinterpret_cast<uint16_t*>(smem + C::IMG_OFF);  // image tile is dead: run-table staging
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
