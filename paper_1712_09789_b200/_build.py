@@ -50,6 +50,8 @@ def _flags(extra: list[str] | None = None) -> list[str]:
     if tile:
         wx, wy = tile.lower().split("x")
         fl += [f"-DCCL_TILE_WX={int(wx)}", f"-DCCL_TILE_WY={int(wy)}"]
+    if os.environ.get("CCL_MINB"):
+        fl += [f"-DCCL_MINB={int(os.environ['CCL_MINB'])}"]
     if os.environ.get("CCL_CLIMB"):
         fl += [f"-DCCL_CLIMB={int(os.environ['CCL_CLIMB'])}"]
     return fl + (extra or [])
@@ -70,7 +72,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     os.makedirs(OUT_DIR, exist_ok=True)
     srcs = sources()
-    tag = (os.environ.get("CCL_TILE", "default") + "_c" + os.environ.get("CCL_CLIMB", "")).replace("x", "_")
+    tag = (os.environ.get("CCL_TILE", "default") + "_c" + os.environ.get("CCL_CLIMB", "") + "_m" + os.environ.get("CCL_MINB", "")).replace("x", "_")
     objs = [os.path.join(OBJ_DIR, os.path.relpath(s, CSRC).replace(os.sep, "__") + f".{tag}.o") for s in srcs]
     jobs = []
     for s, o in zip(srcs, objs):
@@ -85,7 +87,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(r.stdout + r.stderr, file=sys.stderr)
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed:\n" + " ".join(r.args) + "\n" + r.stdout + r.stderr)
-    lib = lib_for_tile(os.environ.get("CCL_TILE") or (("c" + os.environ["CCL_CLIMB"]) if os.environ.get("CCL_CLIMB") else None))
+    exp = "".join(f"{k[4:].lower()}{os.environ[k]}" for k in ("CCL_TILE", "CCL_CLIMB", "CCL_MINB") if os.environ.get(k))
+    lib = lib_for_tile(exp or None)
     if force or jobs or not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
         tmp = lib + ".tmp"
         link = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]

@@ -323,7 +323,7 @@ __device__ __forceinline__ uint32_t walk_root(const node_t* P, uint32_t x, uint3
 
 // ------------------------------------------------------------------ kernel (a)(b)(c)
 template <class C, int VAR, bool TMA>
-__global__ void __launch_bounds__(C::NT, 3) k_local(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img,
+__global__ void __launch_bounds__(C::NT, CCL_MINB) k_local(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img,
                                                     uint32_t* L, uint32_t* work, Geo g) {
     uint8_t* smem = aligned_smem();
     const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
