@@ -199,7 +199,7 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
     // first-overlap path up to CLIMB rows in registers, linking straight to the
     // highest ancestor reached: vertical coarse chains come out CLIMB x shorter.
     {
-        constexpr int CLIMB = 4;
+        constexpr int CLIMB = CCL_CLIMB;
         uint32_t ups[CLIMB];
         ups[0] = um;
 #pragma unroll
@@ -212,18 +212,20 @@ __device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uin
             const uint32_t b = __ffs(t) - 1;
             t &= t - 1;
             uint32_t par = nbase + b;
-            if (VAR == 0) {  // C2FL: run -> ancestor along its first-overlap path
+            if (VAR == 0) {  // C2FL: run -> the run at the top of the vertical fg run
+                             // through its first overlap column (<= CLIMB rows up)
                 const uint32_t mb = m >> b;
-                uint32_t run = (mb & ~(mb + 1u)) << b;
+                const uint32_t ov = ((mb & ~(mb + 1u)) << b) & um;
+                if (ov) {
+                    const uint32_t f = __ffs(ov) - 1;
+                    uint32_t u = um, k = 0;
 #pragma unroll
-                for (int k = 0; k < CLIMB; ++k) {
-                    const uint32_t ov = run & ups[k];
-                    if (!ov) break;
-                    const uint32_t u = ups[k];
-                    const uint32_t s = hi_bit_le(u & ~(u << 1), __ffs(ov) - 1);
-                    par = nbase - uint32_t(k + 1) * C::PS + s;
-                    const uint32_t ub = u >> s;
-                    run = (ub & ~(ub + 1u)) << s;
+                    for (int j = 1; j < CLIMB; ++j) {
+                        const bool up = (k == uint32_t(j - 1)) && ((ups[j] >> f) & 1u);
+                        k = up ? uint32_t(j) : k;
+                        u = up ? ups[j] : u;
+                    }
+                    par = nbase - (k + 1) * C::PS + hi_bit_le(u & ~(u << 1), f);
                 }
             } else if (VAR == 2) {  // CC2FL: pixel -> pixel above
                 if ((um >> b) & 1u) par = nbase + b - C::PS;
