@@ -85,3 +85,76 @@ def test_cpp_dropin(ccl, oracle_mod, tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def _strip_rank(rank, world, port, w, full_h, q):
+    """One rank of the strip protocol on the real kernels (shared GPU, gloo exchange)."""
+    import os
+    import sys
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, REPO)
+    import paper_1712_09789_b200 as ccl
+    from paper_1712_09789_b200.strips import StripLabeler, split_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = ccl.random_image(w, full_h, 0.58, 21)
+        row0, h = split_rows(full_h, world)[rank]
+        dev = torch.device("cuda", 0)
+        d_img = torch.from_numpy(np.ascontiguousarray(img[row0:row0 + h])).to(dev)
+        out = torch.empty((h, w), dtype=torch.uint32, device=dev)
+        lab = StripLabeler(ccl.Context(0), w, h, row0, full_h, rank, world, dev)
+        lab.label(d_img, out)
+        torch.cuda.synchronize()
+        mine = out.cpu().view(torch.int32)
+        hmax = max(hh for _, hh in split_rows(full_h, world))
+        pad = torch.zeros((hmax, w), dtype=torch.int32)
+        pad[:h] = mine
+        parts = [torch.zeros((hmax, w), dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        if rank == 0:
+            got = torch.cat([parts[k][:split_rows(full_h, world)[k][1]] for k in range(world)]).numpy().view(np.uint32)
+            import oracle
+            q.put(bool(np.array_equal(got, oracle.sequential_ccl(img))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strip_labeler_multiprocess(ccl, world):
+    """StripLabeler (the bench's N>1 path) in `world` processes sharing one GPU;
+    the all-gather runs over gloo instead of NCCL (one GPU on the test box)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_strip_rank, args=(r, world, port, 1500, 256 * world + 77, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) is True
+
+
+@pytest.mark.slow
+def test_known_answer_32768(ccl, oracle_mod, known_answers):
+    """Config 5 image on one B200 (5.4 GB working set): K / fg / FNV vs the reference."""
+    import torch
+    ka = known_answers.get("random_32768_d0.5_s0")
+    if ka is None:
+        pytest.skip("known answer not generated")
+    img = torch.from_numpy(ccl.random_image(32768, 32768, 0.5, 0)).cuda()
+    lab = ccl.label_device(img)
+    del img
+    lab = lab.cpu().numpy()
+    k, fg = oracle_mod.count(lab)
+    assert (k, fg) == (ka["K"], ka["fg"])
+    assert f"{oracle_mod.fnv1a64(lab):016x}" == ka["fnv1a64_raw"]
