@@ -21,8 +21,29 @@ OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libccl_b200.so")
 
 
-def lib_for_tile(tile: str | None) -> str:
-    return LIB if not tile else os.path.join(OUT_DIR, f"libccl_b200_{tile}.so")
+def _exp_defs() -> list[str]:
+    """Experiment knobs: CCL_TILE=WXxWY and CCL_DEFS="NAME=V,NAME=V" (e.g.
+    CCL_DEFS=CCL_JUMP=1,CCL_WAVE=1).  A non-default build gets its own library
+    name, so the in-tree default library is never clobbered by an experiment."""
+    fl = []
+    tile = os.environ.get("CCL_TILE")
+    if tile:
+        wx, wy = tile.lower().split("x")
+        fl += [f"-DCCL_TILE_WX={int(wx)}", f"-DCCL_TILE_WY={int(wy)}"]
+    for d in filter(None, os.environ.get("CCL_DEFS", "").split(",")):
+        fl.append("-D" + d.strip())
+    return fl
+
+
+def exp_tag() -> str:
+    t = "_".join(f.replace("-DCCL_", "").replace("=", "").lower() for f in _exp_defs())
+    return t
+
+
+def lib_for_tag(tag: str | None) -> str:
+    return LIB if not tag else os.path.join(OUT_DIR, f"libccl_b200_{tag}.so")
+
+
 OBJ_DIR = os.path.join(REPO, "build", "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -46,14 +67,7 @@ def sources() -> list[str]:
 def _flags(extra: list[str] | None = None) -> list[str]:
     fl = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
                  "-I", os.path.join(REPO, "include"), "-I", CSRC]
-    tile = os.environ.get("CCL_TILE")  # e.g. "8x2" for experiments
-    if tile:
-        wx, wy = tile.lower().split("x")
-        fl += [f"-DCCL_TILE_WX={int(wx)}", f"-DCCL_TILE_WY={int(wy)}"]
-    if os.environ.get("CCL_MINB"):
-        fl += [f"-DCCL_MINB={int(os.environ['CCL_MINB'])}"]
-    if os.environ.get("CCL_CLIMB"):
-        fl += [f"-DCCL_CLIMB={int(os.environ['CCL_CLIMB'])}"]
+    fl += _exp_defs()
     return fl + (extra or [])
 
 
@@ -72,7 +86,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     os.makedirs(OUT_DIR, exist_ok=True)
     srcs = sources()
-    tag = (os.environ.get("CCL_TILE", "default") + "_c" + os.environ.get("CCL_CLIMB", "") + "_m" + os.environ.get("CCL_MINB", "")).replace("x", "_")
+    tag = exp_tag() or "default"
     objs = [os.path.join(OBJ_DIR, os.path.relpath(s, CSRC).replace(os.sep, "__") + f".{tag}.o") for s in srcs]
     jobs = []
     for s, o in zip(srcs, objs):
@@ -87,8 +101,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(r.stdout + r.stderr, file=sys.stderr)
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed:\n" + " ".join(r.args) + "\n" + r.stdout + r.stderr)
-    exp = "".join(f"{k[4:].lower()}{os.environ[k]}" for k in ("CCL_TILE", "CCL_CLIMB", "CCL_MINB") if os.environ.get(k))
-    lib = lib_for_tile(exp or None)
+    lib = lib_for_tag(exp_tag() or None)
     if force or jobs or not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
         tmp = lib + ".tmp"
         link = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]

@@ -420,7 +420,7 @@ void ccl_tile_shape(uint32_t* tw, uint32_t* th) {
     if (th) *th = uint32_t(cclk::tile_h());
 }
 
-int ccl_launches_per_label(void) { return 3; }
+int ccl_launches_per_label(void) { return 4; }  // (a), (d), (d2) resolve, (e)
 
 const char* ccl_last_error(void) { return g_err.c_str(); }
 

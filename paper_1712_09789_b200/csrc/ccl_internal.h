@@ -7,8 +7,11 @@
 #include <stdint.h>
 
 // GPU tile = CCL_TILE_WX x CCL_TILE_WY warps, each warp a 32x32 pixel sub-tile.
-#ifndef CCL_CLIMB
-#define CCL_CLIMB 4  // rows kernel (a) climbs when linking a run upward
+#ifndef CCL_JUMP
+#define CCL_JUMP 2  // pointer-jumping rounds over the coarse forest in kernel (a)
+#endif
+#ifndef CCL_WAVE
+#define CCL_WAVE 0  // barrier between flatten waves in kernel (a)
 #endif
 #ifndef CCL_MINB
 #define CCL_MINB 3  // min resident CTAs of kernel (a) (register cap)

@@ -1,11 +1,15 @@
 // ccl_kernels.cu — the hand-written sm_100a kernels of the labeler.
 //
-//   (a)+(b)+(c)  k_local  : TMA-stage a TW x TH tile, warp-bit run detection
-//                           (coarse row scan), coarse column link, smem
-//                           min-union refinement, flatten (unification).
-//                           Exports, per tile, a compact RUN TABLE (one u16
-//                           local root per row run), the row-word masks and
-//                           the list of seam-touching roots; writes the tile's
+//   (a)+(b)+(c)  k_local  : TMA-stage a TW x TH tile, foreground row words,
+//                           word-level run detection (coarse row scan) with
+//                           runs that continue across 32-px words kept as ONE
+//                           node, COMPACT node ids in tile raster order
+//                           (prefix counts), coarse column links, smem
+//                           min-union refinement, and an id-ordered flatten
+//                           (unification).  Exports, per tile, a run table
+//                           (one u16 per node: local root position, or the
+//                           rank of a seam-touching root), the row-word masks
+//                           and the seam-touching root list; writes the tile's
 //                           seam pixels and registers the seam-touching roots
 //                           as nodes of the global forest in the label buffer.
 //   (d)          k_seams  : boundary-only pass (Algorithm 2): one thread per
@@ -14,8 +18,12 @@
 //   (e)          k_final  : resolves each seam-touching root ONCE through the
 //                           global forest, expands the run table to pixels and
 //                           writes every label exactly once (swizzled TMA
-//                           stores).  It never re-reads the image: masks
-//                           (0.125 B/px) + run table (~0.5 B/px at d=0.5).
+//                           stores).  It never re-reads the image.
+//
+// Node ids are assigned in tile raster order, so the min-id root of a class is
+// its min raster position (forest.hpp:44-111 invariant parent <= self), which
+// is the component's min pixel: the reference's canonical label
+// (image.hpp:41-43) after convert_ids (local_labeler.cpp:102-112).
 //
 // The reference's block config / variant are honoured for validation and
 // strategy selection; the GPU tile is an internal constant (labels are
@@ -33,41 +41,62 @@ template <int WX_, int WY_>
 struct Cfg {
     static constexpr int WX = WX_, WY = WY_;
     static constexpr int TW = 32 * WX, TH = 32 * WY, NT = 32 * WX * WY, NWARP = WX * WY;
-    static constexpr int PS = TW + 1;  // padded node row stride: node id order == raster order
-    static constexpr int NODES = TH * PS;
-    static constexpr int FW = (NODES + 31) / 32;
-    static constexpr int P_BYTES = ((NODES * 2 + 1023) / 1024) * 1024;  // u16 parents
-    static constexpr int F_OFF = P_BYTES;
-    static constexpr int M_OFF = F_OFF + ((FW * 4 + 127) / 128) * 128;
-    static constexpr int IMG_OFF = M_OFF + ((TH * WX * 4 + 127) / 128) * 128;
-    static constexpr int FR_OFF = IMG_OFF + TW * TH;
-    static constexpr int BAR_OFF = FR_OFF + ((4 * (1 + TW + 2 * TH) + 127) / 128) * 128;
-    static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
-    // work buffer (global) per tile
-    static constexpr int MASK_WORDS = TH * WX;                    // row-word masks
-    static constexpr int MAXF = TW + 2 * TH;                      // bound on seam-touching roots
-    static constexpr int HDR_WORDS = ((1 + NWARP + MAXF) + 3) / 4 * 4;  // nF, run count per warp, F list
-    static constexpr int TBL_PER_WARP = 512;                      // u16 run entries (<= 16 runs x 32 rows)
-    // kernel (e) smem
-    static constexpr int E_M_OFF = 0;
-    static constexpr int E_HDR_OFF = E_M_OFF + MASK_WORDS * 4;
-    static constexpr int E_FT_OFF = E_HDR_OFF + HDR_WORDS * 4;
-    static constexpr int E_TBL_OFF = E_FT_OFF + MAXF * 4;
-    static constexpr int E_STG_OFF = ((E_TBL_OFF + NWARP * TBL_PER_WARP * 2) + 1023) / 1024 * 1024;
-    static constexpr int E_BAR_OFF = E_STG_OFF + NWARP * 4096;
-    static constexpr int E_SMEM = E_BAR_OFF + 64 + 1024;
+    static constexpr int PX = TW * TH;
+    static constexpr int MAXF = 2 * TW + 2 * TH;  // bound on seam-touching roots (one per boundary run)
+    // work buffer (global) per tile, in u32 words:
+    //   head [nF, nodes, -, -] | row-word masks | per-word node prefix (u16) |
+    //   seam-root list (global index; resolved label after k_resolve) |
+    //   seam records (local root of every border pixel: top, bottom, left, right) | node table (u16)
+    static constexpr int MW = TH * WX;  // row words
+    static constexpr int W_HEAD = 0;
+    static constexpr int W_MASK = 4;
+    static constexpr int W_PF = W_MASK + MW;
+    static constexpr int W_LIST = W_PF + MW / 2;
+    static constexpr int W_REC = W_LIST + MAXF;
+    static constexpr int W_TBL = W_REC + 2 * TW + 2 * TH;
+    static constexpr int TILE_WORDS = W_TBL + PX / 2;  // table sized for pixel nodes (worst case)
+    static constexpr int S1_BYTES = (W_LIST - W_HEAD) * 4;  // head + masks + prefixes: one bulk copy
     static_assert(TW <= 256 && TH <= 256, "TMA box dims are limited to 256");
-    static_assert(NWARP * TBL_PER_WARP * 2 <= TW * TH, "run-table staging must fit in the image area");
-    static_assert(NODES < 0x8000, "node ids must leave bit 15 free for the seam-root tag");
+    static_assert(PX <= 0x8000, "positions must leave bit 15 free for the seam-root tag");
+    static_assert(MW % 8 == 0, "16-byte alignment of the work-buffer sections");
 };
 
 using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
 
-// Node parents are u16 (node ids < 2^15; bit 15 tags seam roots): half the
-// shared memory of u32 parents -> more resident CTAs for this latency-bound
-// phase.  Unions are CAS min-unions on the 16-bit entries.
-using node_t = uint16_t;
+// Kernel (a) shared memory, per node granularity (runs: <= PX/2 nodes).
+template <class C, bool RUNS>
+struct ALayout {
+    static constexpr int MAXN = RUNS ? C::PX / 2 : C::PX;
+    static constexpr int P_OFF = 0;                                        // u16 parents, then the table
+    static constexpr int POS_OFF = P_OFF + MAXN * 2;                       // u16 node position / seam tag
+    static constexpr int FB_OFF = POS_OFF + MAXN * 2;                      // seam-root bitmap
+    static constexpr int M_OFF = FB_OFF + ((MAXN / 32 * 4 + 127) / 128) * 128;  // row-word masks
+    static constexpr int PF16_OFF = M_OFF + C::MW * 4;                     // u16 prefixes (contiguous: one bulk store)
+    static constexpr int PF_OFF = PF16_OFF + C::MW * 2;                    // u32 counts / prefixes
+    static constexpr int BT_OFF = PF_OFF + C::MW * 4;                      // band totals (+ total)
+    static constexpr int FR_OFF = BT_OFF + 128;                            // [count, root ids -> global idx]
+    static constexpr int IMG_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
+    static constexpr int BAR_OFF = IMG_OFF + C::PX;
+    static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
+};
+
+// Kernel (e) shared memory: 3 head/mask stages, 2 table/label stages, staging.
+template <class C, bool RUNS>
+struct ELayout {
+    static constexpr int S1 = (C::S1_BYTES + 127) / 128 * 128;
+    static constexpr int TBLB = RUNS ? C::PX : 2 * C::PX;                 // u16 node table
+    static constexpr int S2 = (C::MAXF * 4 + TBLB + 127) / 128 * 128;     // resolved labels + table
+    static constexpr int S1_OFF = 0;
+    static constexpr int S2_OFF = S1_OFF + 3 * S1;
+    static constexpr int STG_OFF = ((S2_OFF + 2 * S2) + 1023) / 1024 * 1024;
+    static constexpr int BAR_OFF = STG_OFF + C::NWARP * 4096;
+    static constexpr int SMEM = BAR_OFF + 64 + 1024;
+};
+
 constexpr uint32_t kTag = 0x8000u;
+
+// Node parents are u16; unions are CAS min-unions on the 16-bit entries.
+using node_t = uint16_t;
 __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
     volatile node_t* vP = P;
     uint32_t p = vP[x];
@@ -97,19 +126,22 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 }
 
-// Work-buffer views of one tile (tile index tg over frames x tile rows x tile cols).
+// Work-buffer view of one tile (tile index tg over frames x tile rows x tile cols).
 template <class C>
-struct Work {
-    uint32_t* masks;
-    uint32_t* hdr;
-    uint16_t* tbl;
-    __device__ __forceinline__ Work(uint32_t* work, size_t ntiles, size_t tg) {
-        masks = work + tg * C::MASK_WORDS;
-        hdr = work + ntiles * C::MASK_WORDS + tg * C::HDR_WORDS;
-        tbl = reinterpret_cast<uint16_t*>(work + ntiles * (C::MASK_WORDS + C::HDR_WORDS)) +
-              tg * size_t(C::NWARP * C::TBL_PER_WARP);
-    }
+__device__ __forceinline__ uint32_t* work_tile(uint32_t* work, size_t tg) {
+    return work + tg * size_t(C::TILE_WORDS);
+}
+
+// Linear tile index -> (tx, ty, frame).
+struct TileId {
+    uint32_t tx, ty, fz;
 };
+__device__ __forceinline__ TileId tile_of(uint32_t t, const Geo& g) {
+    const uint32_t per = g.ntx * g.nty;
+    const uint32_t fz = t / per, r = t - fz * per;
+    const uint32_t ty = r / g.ntx;
+    return TileId{r - ty * g.ntx, ty, fz};
+}
 
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
@@ -123,453 +155,577 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
                  : "memory");
 }
 
-// Per-lane result of the tile-local phase.
-struct LaneState {
-    uint32_t m;         // foreground bits of this lane's 32-px row word
-    uint32_t st;        // segment (node) starts in the word
-    uint32_t rootmask;  // segment starts that are local roots
-};
+// Node starts of one row word: runs (a run continuing from the word on its
+// left is not restarted, so a tile-row run is ONE node) or fg pixels.
+template <bool RUNS>
+__device__ __forceinline__ uint32_t word_starts(uint32_t m, uint32_t lm) {
+    if (!RUNS) return m;
+    const uint32_t cont = (lm >> 31) & m & 1u;
+    return m & ~((m << 1) | cont);
+}
 
-// Steps 1-3 of Algorithm 1 for one tile, fully in shared memory.  On return
-// (after a __syncthreads): P[s] == local root for every segment start s, and
-// the F bitmap flags every local root whose component touches a tile side
-// that faces another tile (or another strip).
+// Raster-order node prefix of every row word of the tile.  Each lane owns
+// word (row, wx) with `cnt` node starts; CNT is scratch for the counts.
+// Returns the number of nodes that start before this word; *total = nodes in
+// the tile.  Two barriers (one when the tile is a single warp row).
+template <class C>
+__device__ __forceinline__ uint32_t tile_prefix(uint32_t cnt, uint32_t* CNT, uint32_t* BT, int row, int wx, int wy,
+                                                int lane, uint32_t* total) {
+    CNT[row * C::WX + wx] = cnt;
+    __syncthreads();
+    uint32_t left = 0, rowtot = 0;
+#pragma unroll
+    for (int w = 0; w < C::WX; ++w) {
+        const uint32_t c = CNT[row * C::WX + w];
+        left += (w < wx) ? c : 0u;
+        rowtot += c;
+    }
+    uint32_t inc = rowtot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    uint32_t band = 0, tot;
+    if (C::WY == 1) {
+        tot = __shfl_sync(0xffffffffu, inc, 31);
+    } else {
+        if (wx == 0 && lane == 31) BT[wy] = inc;
+        __syncthreads();
+        tot = 0;
+#pragma unroll
+        for (int b = 0; b < C::WY; ++b) {
+            const uint32_t t = BT[b];
+            band += (b < wy) ? t : 0u;
+            tot += t;
+        }
+    }
+    *total = tot;
+    return band + inc - rowtot + left;
+}
+
+// Id of the node holding bit b of a word with starts st and prefix pfx (a bit
+// before the word's first start belongs to the node continuing from the left).
+__device__ __forceinline__ uint32_t node_of(uint32_t pfx, uint32_t st, uint32_t b) {
+    return pfx + __popc(st & (0xFFFFFFFFu >> (31u - b))) - 1u;
+}
+// Bits b of o such that some bit of o lies strictly below b inside the same
+// run of m (o must be a subset of m): the carry-in vector of m + o, within m.
+__device__ __forceinline__ uint32_t lower_in_run(uint32_t m, uint32_t o) {
+    return ((m + o) ^ m ^ o) & m;
+}
+
+template <class C>
+__device__ __forceinline__ uint32_t pos_gidx(uint32_t pos, uint32_t x0, uint32_t y0, const Geo& g) {
+    constexpr int SH = __builtin_ctz(C::TW);
+    return (g.row0 + y0 + (pos >> SH)) * g.W + x0 + (pos & (C::TW - 1));  // global raster index (convert_ids)
+}
+
+// ------------------------------------------------------------------ kernel (a)(b)(c)
+// Persistent: CTA b labels tiles b, b + G, b + 2G, ... (G = gridDim.x).  The
+// next tile's image is TMA-loaded into the staging buffer as soon as the
+// current tile's masks are built, so the load overlaps a whole tile of work.
 template <class C, int VAR, bool TMA>
-__device__ __forceinline__ LaneState tile_local(const CUtensorMap* tm, const uint8_t* img, const Geo& g,
-                                                uint32_t tx, uint32_t ty, uint32_t fz, uint8_t* smem) {
-    node_t* P = reinterpret_cast<node_t*>(smem);
-    uint32_t* F = reinterpret_cast<uint32_t*>(smem + C::F_OFF);
-    uint32_t* M = reinterpret_cast<uint32_t*>(smem + C::M_OFF);
-    uint8_t* IMG = smem + C::IMG_OFF;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+__global__ void __launch_bounds__(C::NT, CCL_MINB)
+    k_local(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img, uint32_t* L, uint32_t* work, Geo g,
+            uint32_t ntiles) {
+    constexpr bool RUNS = (VAR == 0 || VAR == 1);
+    using A = ALayout<C, RUNS>;
+    uint8_t* smem = aligned_smem();
+    node_t* P = reinterpret_cast<node_t*>(smem + A::P_OFF);
+    uint16_t* POS = reinterpret_cast<uint16_t*>(smem + A::POS_OFF);
+    uint32_t* FB = reinterpret_cast<uint32_t*>(smem + A::FB_OFF);
+    uint32_t* M = reinterpret_cast<uint32_t*>(smem + A::M_OFF);
+    uint16_t* PF16 = reinterpret_cast<uint16_t*>(smem + A::PF16_OFF);
+    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::PF_OFF);
+    uint32_t* BT = reinterpret_cast<uint32_t*>(smem + A::BT_OFF);
+    uint32_t* FR = reinterpret_cast<uint32_t*>(smem + A::FR_OFF);
+    uint8_t* IMG = smem + A::IMG_OFF;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
+
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane;
     const int col0 = wx * 32;
-    const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
 
-    // ---- stage the tile and build the row-word foreground masks
-    if (TMA) {
-        if (tid == 0) {
-            mbar_init(bar, 1);
-            mbar_expect_tx(bar, C::TW * C::TH);
-            tma_load_3d(IMG, tm, int(x0), int(y0), int(fz), bar);  // OOB -> 0 == background
-        }
+    auto issue = [&](uint32_t t) {  // TMA 2-D tile load, OOB -> 0 == background
+        const TileId q = tile_of(t, g);
+        mbar_expect_tx(bar, C::PX);
+        tma_load_3d(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar);
+    };
+    if (TMA && tid == 0) {
+        prefetch_tmap(&tm_img);
+        mbar_init(bar, 1);
+        if (blockIdx.x < ntiles) issue(blockIdx.x);
     }
-    for (int i = tid; i < C::FW; i += C::NT) F[i] = 0u;
-    if (tid == 0) *reinterpret_cast<uint32_t*>(smem + C::FR_OFF) = 0u;
-    uint32_t m;
-    if (TMA) {
-        __syncthreads();  // mbarrier init visible before anyone polls it
-        mbar_wait(bar, 0);
-        constexpr int CPR = C::TW / 16;
-        uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
-#pragma unroll
-        for (int c = tid; c < C::TH * CPR; c += C::NT) {
-            const uint4 q = *reinterpret_cast<const uint4*>(IMG + c * 16);
-            M16[c] = static_cast<uint16_t>(eq1_mask16(q));
-        }
+
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const TileId ti = tile_of(t, g);
+        const uint32_t tx = ti.tx, ty = ti.ty;
+        const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
+        uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;  // strip/frame-local index = global - base
+        uint32_t* wt = work_tile<C>(work, t);
+
+        // the previous tile's bulk stores must have read P / M / PF16, and its
+        // last phase must be done with every smem array
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
-        m = M[row * C::WX + wx];
-    } else {
-        m = 0u;
-        const uint32_t gy = y0 + row;
-        if (gy < g.H) {
-            const uint8_t* src = img + size_t(fz) * g.frame_pitch + size_t(gy) * g.img_pitch;
-            for (int b = 0; b < 32; ++b) {
-                const uint32_t gx = x0 + col0 + b;
-                if (gx < g.W && src[gx] == 1) m |= 1u << b;
+        for (int i = tid; i < A::MAXN / 32; i += C::NT) FB[i] = 0u;
+        if (tid == 0) FR[0] = 0u;
+
+        // ---- row-word foreground masks (byte == 1)
+        if (TMA) {
+            mbar_wait(bar, it & 1u);
+            constexpr int CPR = C::TW / 16;
+            uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
+#pragma unroll
+            for (int c = tid; c < C::TH * CPR; c += C::NT) {
+                const uint4 q = *reinterpret_cast<const uint4*>(IMG + c * 16);
+                M16[c] = static_cast<uint16_t>(eq1_mask16(q));
             }
-        }
-        M[row * C::WX + wx] = m;
-        __syncthreads();
-    }
-
-    // ---- coarse row scan: word-local runs are the nodes (pixel nodes for CC2FL/NC2FL)
-    constexpr bool RUNS = (VAR == 0 || VAR == 1);
-    const uint32_t st = RUNS ? (m & ~(m << 1)) : m;
-    uint32_t um = __shfl_up_sync(0xffffffffu, m, 1);
-    if (lane == 0) um = (wy > 0) ? M[(row - 1) * C::WX + wx] : 0u;
-    const uint32_t ust = RUNS ? (um & ~(um << 1)) : um;
-    const uint32_t nbase = uint32_t(row * C::PS + col0);
-
-    // ---- init + coarse column scan (no atomics: plain parent links upward).
-    // C2FL links a run to the first run above it that it overlaps -- and, since
-    // the masks of the rows above are at hand (shuffles), keeps climbing that
-    // first-overlap path up to CLIMB rows in registers, linking straight to the
-    // highest ancestor reached: vertical coarse chains come out CLIMB x shorter.
-    {
-        constexpr int CLIMB = CCL_CLIMB;
-        uint32_t ups[CLIMB];
-        ups[0] = um;
-#pragma unroll
-        for (int k = 1; k < CLIMB; ++k) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, m, k + 1);
-            ups[k] = lane > k ? v : 0u;  // rows above this warp's band are not climbed
-        }
-        uint32_t t = st;
-        while (t) {
-            const uint32_t b = __ffs(t) - 1;
-            t &= t - 1;
-            uint32_t par = nbase + b;
-            if (VAR == 0) {  // C2FL: run -> the run at the top of the vertical fg run
-                             // through its first overlap column (<= CLIMB rows up)
-                const uint32_t mb = m >> b;
-                const uint32_t ov = ((mb & ~(mb + 1u)) << b) & um;
-                if (ov) {
-                    const uint32_t f = __ffs(ov) - 1;
-                    uint32_t u = um, k = 0;
-#pragma unroll
-                    for (int j = 1; j < CLIMB; ++j) {
-                        const bool up = (k == uint32_t(j - 1)) && ((ups[j] >> f) & 1u);
-                        k = up ? uint32_t(j) : k;
-                        u = up ? ups[j] : u;
-                    }
-                    par = nbase - (k + 1) * C::PS + hi_bit_le(u & ~(u << 1), f);
+        } else {
+            uint32_t mm = 0u;
+            const uint32_t gy = y0 + row;
+            if (gy < g.H) {
+                const uint8_t* src = img + size_t(ti.fz) * g.frame_pitch + size_t(gy) * g.img_pitch;
+                for (int b = 0; b < 32; ++b) {
+                    const uint32_t gx = x0 + col0 + b;
+                    if (gx < g.W && src[gx] == 1) mm |= 1u << b;
                 }
-            } else if (VAR == 2) {  // CC2FL: pixel -> pixel above
-                if ((um >> b) & 1u) par = nbase + b - C::PS;
             }
-            P[nbase + b] = node_t(par);
+            M[row * C::WX + wx] = mm;
         }
-    }
-    __syncthreads();
+        __syncthreads();
+        if (TMA && tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x);  // staging buffer is dead
 
-    // ---- refinement: min-union of the adjacencies the coarse scans did not link
-    if (RUNS) {
-        const uint32_t o = m & um;
-        uint32_t U = o & ~(o << 1);                   // one pair per overlapping (run, upper run)
-        if (VAR == 0) U &= has_lower_in_run(m, o);   // first overlap already linked by the column scan
-        while (U) {
-            const uint32_t b = __ffs(U) - 1;
-            U &= U - 1;
-            nunion(P, nbase + hi_bit_le(st, b), nbase - C::PS + hi_bit_le(ust, b));
+        const uint32_t m = M[row * C::WX + wx];
+        const uint32_t lm = wx > 0 ? M[row * C::WX + wx - 1] : 0u;
+        const uint32_t um = row > 0 ? M[(row - 1) * C::WX + wx] : 0u;
+        const uint32_t lum = (row > 0 && wx > 0) ? M[(row - 1) * C::WX + wx - 1] : 0u;
+        const uint32_t st = word_starts<RUNS>(m, lm);
+        const uint32_t ust = word_starts<RUNS>(um, lum);
+
+        // ---- coarse row scan: node ids in tile raster order
+        uint32_t nodes;
+        const uint32_t pfx = tile_prefix<C>(__popc(st), CNT, BT, row, wx, wy, lane, &nodes);
+        PF16[row * C::WX + wx] = uint16_t(pfx);
+        uint32_t upfx = __shfl_up_sync(0xffffffffu, pfx, 1);
+        if (lane == 0) {  // word above belongs to the warp band above: prefix from the counts
+            uint32_t rest = 0, left = 0;
+#pragma unroll
+            for (int w = 0; w < C::WX; ++w) {
+                rest += (row > 0 && w >= wx) ? CNT[(row - 1) * C::WX + w] : 0u;
+                left += (w < wx) ? CNT[row * C::WX + w] : 0u;
+            }
+            upfx = pfx - left - rest;
         }
-    } else {
-        if (VAR == 3) {  // NC2FL: every vertical pair
-            uint32_t U = m & um;
+        const uint32_t rowpos = uint32_t(row * C::TW + col0);
+
+        // ---- init + coarse column scan (plain stores, no atomics): every node is
+        // its own parent, except that C2FL links a run to the upper run holding
+        // its first overlap inside this word and CC2FL links a pixel to the pixel above.
+        const uint32_t o = m & um;
+        const uint32_t ocont = (o & 1u) & ((lm & lum) >> 31);  // overlap continuing from the left word
+        const uint32_t os = (o & ~(o << 1)) & ~ocont;          // one bit per (node, upper node) overlap
+        uint32_t first = 0u;                                   // overlaps handled by a coarse link
+        if (VAR == 0) first = os & ~lower_in_run(m, o) & ~((st & 1u) ? 0u : (m & ~(m + 1u)));
+        if (VAR == 2) first = o;
+        {
+            uint32_t tt = st, id = pfx;
+            while (tt) {
+                const uint32_t b = __ffs(tt) - 1;
+                tt &= tt - 1;
+                uint32_t par = id;
+                if (VAR == 0) {
+                    const uint32_t fb = first & (0xFFFFFFFFu << b);  // first overlaps at/after this run
+                    const uint32_t f = __ffs(fb) - 1;
+                    const uint32_t nxt = tt ? __ffs(tt) - 1 : 32u;   // next run start in this word
+                    if (fb && f < nxt) par = node_of(upfx, ust, f);
+                } else if (VAR == 2) {
+                    if ((um >> b) & 1u) par = node_of(upfx, ust, b);
+                }
+                P[id] = node_t(par);
+                POS[id] = uint16_t(rowpos + b);
+                ++id;
+            }
+        }
+        __syncthreads();
+
+        // ---- pointer jumping over the coarse forest (balanced over node ids):
+        // coarse links form vertical chains; each round halves their length.
+        if (VAR == 0 || VAR == 2) {
+#pragma unroll 1
+            for (int j = 0; j < CCL_JUMP; ++j) {
+                volatile node_t* vP = P;
+                for (uint32_t id = tid; id < nodes; id += C::NT) {
+                    const uint32_t p = vP[id];
+                    const uint32_t pp = vP[p];
+                    if (pp != p) vP[id] = node_t(pp);
+                }
+                __syncthreads();
+            }
+        }
+
+        // ---- refinement: min-union of the adjacencies the coarse scans did not link
+        {
+            uint32_t U;
+            if (RUNS) U = os & ~first;           // remaining (run, upper run) overlaps
+            else U = (VAR == 3) ? o : 0u;        // NC2FL: every vertical pixel pair
             while (U) {
                 const uint32_t b = __ffs(U) - 1;
                 U &= U - 1;
-                nunion(P, nbase + b, nbase + b - C::PS);
+                nunion(P, node_of(pfx, st, b), node_of(upfx, ust, b));
             }
-        }
-        uint32_t hp = (m & (m << 1)) & ~(um & (um << 1));  // row pairs, minus closed 2x2 squares
-        while (hp) {
-            const uint32_t b = __ffs(hp) - 1;
-            hp &= hp - 1;
-            nunion(P, nbase + b, nbase + b - 1);
-        }
-    }
-    if (wx > 0 && (m & 1u)) {  // run continuing across the word boundary
-        const uint32_t lm = M[row * C::WX + wx - 1];
-        if (lm >> 31) {
-            const uint32_t lst = RUNS ? (lm & ~(lm << 1)) : lm;
-            nunion(P, nbase, nbase - 32 + (31 - __clz(lst)));
-        }
-    }
-    __syncthreads();
-
-    // ---- seam-touching roots (components reaching a side that faces a
-    // neighbour tile/strip): marked once via the F bitmap, ranked by arrival
-    // and TAGGED in their own entry (0x8000 | rank) after a barrier, so a
-    // single read-only walk per run later yields either an interior root or
-    // the rank of a seam root.  No whole-tile flatten pass is needed.
-    const bool has_top = ty > 0 || g.edge_above;
-    const bool has_bot = ty + 1 < g.nty || g.edge_below;
-    const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
-    uint32_t* FR = reinterpret_cast<uint32_t*>(smem + C::FR_OFF);  // [0] = count, [1..] = roots
-    auto mark = [&](uint32_t n) {
-        const uint32_t x = nfind(P, n);
-        const uint32_t bit = 1u << (x & 31);
-        if (!(atomicOr(&F[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
-    };
-    if (wy == 0 && has_top) {
-        const uint32_t s0 = __shfl_sync(0xffffffffu, st, 0);
-        if ((s0 >> lane) & 1u) mark(col0 + lane);
-    }
-    if (wy == C::WY - 1 && has_bot) {
-        const uint32_t sl = __shfl_sync(0xffffffffu, st, 31);
-        if ((sl >> lane) & 1u) mark((C::TH - 1) * C::PS + col0 + lane);
-    }
-    if (wx == 0 && has_left && (m & 1u)) mark(nbase);
-    if (wx == C::WX - 1 && has_right && (m >> 31)) mark(nbase + hi_bit_le(st, 31));
-    __syncthreads();
-    const uint32_t nf = FR[0];
-    for (uint32_t k = tid; k < nf; k += C::NT) P[FR[1 + k]] = node_t(kTag | k);
-    __syncthreads();
-    const uint32_t rootmask = 0u;
-    return LaneState{m, st, rootmask};
-}
-
-template <class C>
-__device__ __forceinline__ uint32_t node_gidx(uint32_t node, uint32_t x0, uint32_t y0, const Geo& g) {
-    const uint32_t r = node / C::PS;
-    const uint32_t c = node - r * C::PS;
-    return (g.row0 + y0 + r) * g.W + x0 + c;  // global raster index (convert_ids)
-}
-
-// Read-only walk to a run's root after tagging: returns the root node id and
-// sets `tag` to 0x8000|rank for seam-touching roots (0 otherwise).
-// (Path halving here was measured: it shortens spiral chains but costs more
-// than it saves on random d=0.5 tiles, whose chains are short.)
-__device__ __forceinline__ uint32_t walk_root(const node_t* P, uint32_t x, uint32_t& tag) {
-    uint32_t p = P[x];
-    while (p != x && !(p & kTag)) {
-        x = p;
-        p = P[x];
-    }
-    tag = (p & kTag) ? p : 0u;
-    return x;
-}
-
-// ------------------------------------------------------------------ kernel (a)(b)(c)
-template <class C, int VAR, bool TMA>
-__global__ void __launch_bounds__(C::NT, CCL_MINB) k_local(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img,
-                                                    uint32_t* L, uint32_t* work, Geo g) {
-    uint8_t* smem = aligned_smem();
-    const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
-    if (TMA && threadIdx.x == 0) prefetch_tmap(&tm_img);
-    const LaneState s = tile_local<C, VAR, TMA>(&tm_img, img, g, tx, ty, fz, smem);
-    node_t* P = reinterpret_cast<node_t*>(smem);
-    const uint32_t* M = reinterpret_cast<const uint32_t*>(smem + C::M_OFF);
-    uint16_t* STG = reinterpret_cast<uint16_t*>(smem + C::IMG_OFF);  // image tile is dead: run-table staging
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wx = warp % C::WX, wy = warp / C::WX;
-    const int row = wy * 32 + lane, col0 = wx * 32;
-    const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
-    const uint32_t nbase = uint32_t(row * C::PS + col0);
-    uint32_t* Lf = L + size_t(fz) * g.frame_px;  // strip/frame-local index = global - base
-    const size_t ntiles = size_t(g.ntx) * g.nty * gridDim.z;
-    const Work<C> wk(work, ntiles, (size_t(fz) * g.nty + ty) * g.ntx + tx);
-
-    const uint32_t* FR = reinterpret_cast<const uint32_t*>(smem + C::FR_OFF);
-    const uint32_t nf = FR[0];
-    if (tid == 0) wk.hdr[0] = nf;
-    // run table: one u16 per row run, in (row, run) order per warp; seam-touching
-    // roots carry 0x8000 | rank (the index into this tile's seam-root list)
-    const uint32_t rst = s.m & ~(s.m << 1);
-    const uint32_t cnt = __popc(rst);
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    {
-        uint16_t* dst = STG + warp * C::TBL_PER_WARP + (inc - cnt);
-        uint32_t t = rst;
-        while (t) {
-            const uint32_t b = __ffs(t) - 1;
-            t &= t - 1;
-            uint32_t tag;
-            const uint32_t r = walk_root(P, nbase + b, tag);
-            *dst++ = tag ? uint16_t(0x8000u | (tag & 0x7FFFu)) : uint16_t(r);
-        }
-    }
-    if (lane == 0) wk.hdr[1 + warp] = total;
-    // seam-root list (global raster indices, rank order) + forest registration L[g] = g
-    for (uint32_t k = tid; k < nf; k += C::NT) {
-        const uint32_t gi = node_gidx<C>(FR[1 + k], x0, y0, g);
-        wk.hdr[1 + C::NWARP + k] = gi;
-        Lf[gi - g.base] = gi;
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0 && total) bulk_store(wk.tbl + warp * C::TBL_PER_WARP, STG + warp * C::TBL_PER_WARP, (total * 2 + 15) & ~15u);
-    __syncthreads();
-    if (tid == 0) bulk_store(wk.masks, M, C::MASK_WORDS * 4);
-    if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-
-    // seam pixels: their local root (global index) or background
-    const bool has_top = ty > 0 || g.edge_above;
-    const bool has_bot = ty + 1 < g.nty || g.edge_below;
-    const uint32_t gx = x0 + col0 + lane;
-    if (wy == 0 && has_top) {
-        const uint32_t m0 = __shfl_sync(0xffffffffu, s.m, 0), s0 = __shfl_sync(0xffffffffu, s.st, 0);
-        if (gx < g.W) {
-            uint32_t v = kBG;
-            if ((m0 >> lane) & 1u) { uint32_t tg; v = node_gidx<C>(walk_root(P, col0 + hi_bit_le(s0, lane), tg), x0, y0, g); }
-            Lf[size_t(y0) * g.W + gx] = v;
-        }
-    }
-    if (wy == C::WY - 1 && has_bot) {
-        const uint32_t ml = __shfl_sync(0xffffffffu, s.m, 31), sl = __shfl_sync(0xffffffffu, s.st, 31);
-        if (gx < g.W) {
-            uint32_t v = kBG;
-            if ((ml >> lane) & 1u) { uint32_t tg; v = node_gidx<C>(walk_root(P, (C::TH - 1) * C::PS + col0 + hi_bit_le(sl, lane), tg), x0, y0, g); }
-            Lf[size_t(y0 + C::TH - 1) * g.W + gx] = v;
-        }
-    }
-    const uint32_t gy = y0 + row;
-    if (gy < g.H) {
-        if (wx == 0 && tx > 0) {
-            uint32_t tg; const uint32_t v = (s.m & 1u) ? node_gidx<C>(walk_root(P, nbase, tg), x0, y0, g) : kBG;
-            Lf[size_t(gy) * g.W + x0] = v;
-        }
-        if (wx == C::WX - 1 && tx + 1 < g.ntx) {
-            uint32_t tg; const uint32_t v = (s.m >> 31) ? node_gidx<C>(walk_root(P, nbase + hi_bit_le(s.st, 31), tg), x0, y0, g) : kBG;
-            Lf[size_t(gy) * g.W + x0 + C::TW - 1] = v;
-        }
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-
-// ------------------------------------------------------------------ kernel (d)
-// One thread per interior seam pixel pair; pairs whose left (resp. upper)
-// neighbour pair is also foreground on both sides join the same two local
-// components and are skipped (one union per overlapping run).
-template <class C>
-__global__ void __launch_bounds__(256) k_seams(uint32_t* L, Geo g) {
-    const uint32_t fz = blockIdx.y;
-    uint32_t* Lf = L + size_t(fz) * g.frame_px;
-    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t nh = uint64_t(g.W) * (g.nty - 1);
-    const uint64_t nv = uint64_t(g.H) * (g.ntx - 1);
-    const int lane = threadIdx.x & 31;
-    uint32_t a = kBG, b = kBG;
-    bool can_dedup = false;
-    size_t p = 0, step = 0;
-    if (t < nh) {
-        const uint32_t k = uint32_t(t / g.W), x = uint32_t(t - uint64_t(k) * g.W);
-        p = size_t((k + 1) * C::TH) * g.W + x;
-        step = 1;  // neighbour pair along the seam is at x-1
-        a = Lf[p];
-        b = Lf[p - g.W];
-        can_dedup = (x % C::TW) != 0;
-    } else if (t - nh < nv) {
-        const uint64_t u = t - nh;
-        const uint32_t k = uint32_t(u / g.H), y = uint32_t(u - uint64_t(k) * g.H);
-        p = size_t(y) * g.W + size_t(k + 1) * C::TW;
-        step = g.W;  // neighbour pair along the seam is at y-1
-        a = Lf[p];
-        b = Lf[p - 1];
-        can_dedup = (y % C::TH) != 0;
-    }
-    const bool fg = (a != kBG) && (b != kBG);
-    bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
-    if (fg && can_dedup && lane == 0) {
-        const size_t q = p - step;
-        prev = (Lf[q] != kBG) && (Lf[q - (step == 1 ? size_t(g.W) : size_t(1))] != kBG);
-    }
-    if (fg && !(can_dedup && prev)) gunion(Lf, g.base, a, b);
-}
-
-// ------------------------------------------------------------------ kernel (e)
-// Reads only the tile's masks + run table + seam-root list (written by (a)),
-// resolves each seam-touching root once through the global forest, expands
-// runs to pixels and writes every label exactly once.
-template <class C, bool TMA_ST>
-__global__ void __launch_bounds__(C::NT, 4) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
-                                                    const uint32_t* work, Geo g) {
-    uint8_t* smem = aligned_smem();
-    uint32_t* M = reinterpret_cast<uint32_t*>(smem + C::E_M_OFF);
-    uint32_t* HDR = reinterpret_cast<uint32_t*>(smem + C::E_HDR_OFF);
-    uint32_t* FT = reinterpret_cast<uint32_t*>(smem + C::E_FT_OFF);
-    uint16_t* TBL = reinterpret_cast<uint16_t*>(smem + C::E_TBL_OFF);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::E_BAR_OFF);
-    const uint32_t tx = blockIdx.x, ty = blockIdx.y, fz = blockIdx.z;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wx = warp % C::WX, wy = warp / C::WX;
-    const int row = wy * 32 + lane;
-    const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
-    uint32_t* Lf = L + size_t(fz) * g.frame_px;
-    const size_t ntiles = size_t(g.ntx) * g.nty * gridDim.z;
-    const Work<C> wk(const_cast<uint32_t*>(work), ntiles, (size_t(fz) * g.nty + ty) * g.ntx + tx);
-
-    if (tid == 0) {
-        if (TMA_ST) prefetch_tmap(&tm_lab);
-        mbar_init(bar, 1);
-        mbar_expect_tx(bar, (C::MASK_WORDS + C::HDR_WORDS) * 4);
-        bulk_load(M, wk.masks, C::MASK_WORDS * 4, bar);
-        bulk_load(HDR, wk.hdr, C::HDR_WORDS * 4, bar);
-    }
-    __syncthreads();
-    mbar_wait(bar, 0);
-    const uint32_t m = M[row * C::WX + wx];
-    const uint32_t st = m & ~(m << 1);
-    const uint32_t cnt = __popc(st);
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    {   // this warp's run entries -> smem (coalesced 16-byte loads)
-        const uint4* src = reinterpret_cast<const uint4*>(wk.tbl + warp * C::TBL_PER_WARP);
-        uint4* dst = reinterpret_cast<uint4*>(TBL + warp * C::TBL_PER_WARP);
-        for (uint32_t i = lane; i < (total * 2 + 15) / 16; i += 32) dst[i] = __ldg(src + i);
-    }
-    // each seam-touching root resolved once through the global forest
-    const uint32_t nF = HDR[0];
-    for (uint32_t k = tid; k < nF; k += C::NT) FT[k] = gfind_ro(Lf, g.base, HDR[1 + C::NWARP + k]);
-    __syncthreads();
-
-    // run labels at the run starts of this lane's staging row, then expand
-    uint8_t* stg = smem + C::E_STG_OFF + warp * 4096;  // 32 x 32 u32, 128B-swizzled
-    uint8_t* myrow = stg + lane * 128;
-    const int sw = lane & 7;
-    {
-        const uint16_t* e = TBL + warp * C::TBL_PER_WARP + (inc - cnt);
-        uint32_t t = st;
-        while (t) {
-            const uint32_t b = __ffs(t) - 1;
-            t &= t - 1;
-            const uint32_t v = *e++;
-            const uint32_t lab = (v & 0x8000u) ? FT[v & 0x7FFFu] : node_gidx<C>(v, x0, y0, g);
-            *reinterpret_cast<uint32_t*>(myrow + ((((b >> 2) ^ sw) << 4) | ((b & 3) << 2))) = lab;
-        }
-    }
-    uint32_t cur = kBG;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        uint4* p = reinterpret_cast<uint4*>(myrow + ((c ^ sw) << 4));
-        uint4 v = *p;
-        uint32_t a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int i = 4 * c + q;
-            cur = ((st >> i) & 1u) ? a[q] : cur;
-            a[q] = ((m >> i) & 1u) ? cur : kBG;
-        }
-        if (TMA_ST) {
-            *p = make_uint4(a[0], a[1], a[2], a[3]);
-        } else {
-            const uint32_t gy = y0 + row;
-            if (gy < g.H) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t gx = x0 + wx * 32 + 4 * c + q;
-                    if (gx < g.W) Lf[size_t(gy) * g.W + gx] = a[q];
+            if (!RUNS) {  // horizontal pixel pairs (incl. the word boundary), minus closed 2x2 squares
+                const uint32_t hm = m & ((m << 1) | ((lm >> 31) & 1u));
+                const uint32_t hu = um & ((um << 1) | ((lum >> 31) & 1u));
+                uint32_t hp = (VAR == 2) ? (hm & ~hu) : hm;
+                while (hp) {
+                    const uint32_t b = __ffs(hp) - 1;
+                    hp &= hp - 1;
+                    const uint32_t id = node_of(pfx, st, b);
+                    nunion(P, id, id - 1);  // the left neighbour is the previous fg pixel in raster order
                 }
             }
         }
-    }
-    if (TMA_ST) {
+        __syncthreads();
+
+        // ---- unification: flatten in id order (parents always have smaller ids)
+        {
+            volatile node_t* vP = P;
+            for (uint32_t id = tid; id < nodes; id += C::NT) {
+                uint32_t r = vP[id];
+                if (r != id) {
+                    uint32_t rr = vP[r];
+                    while (rr != r) {
+                        r = rr;
+                        rr = vP[r];
+                    }
+                    vP[id] = node_t(r);
+                }
+            }
+        }
+
+        // ---- seam-touching roots (components reaching a side that faces a
+        // neighbour tile/strip): marked once via the FB bitmap and ranked.
+        // Read-only walks: the flatten above may still be running elsewhere.
+        const bool has_top = ty > 0 || g.edge_above;
+        const bool has_bot = ty + 1 < g.nty || g.edge_below;
+        const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
+        auto mark = [&](uint32_t id) {
+            volatile node_t* vP = P;
+            uint32_t x = vP[id], p = vP[x];
+            while (p != x) {
+                x = p;
+                p = vP[x];
+            }
+            const uint32_t bit = 1u << (x & 31);
+            if (!(atomicOr(&FB[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
+        };
+        {
+            const uint32_t top_n = PF16[C::WX];                 // nodes in row 0
+            const uint32_t bot0 = PF16[(C::TH - 1) * C::WX];    // first node of the last row
+            if (has_top)
+                for (uint32_t id = tid; id < top_n; id += C::NT) mark(id);
+            if (has_bot)
+                for (uint32_t id = bot0 + tid; id < nodes; id += C::NT) mark(id);
+            if (tid < C::TH) {
+                const int r = tid;
+                if (has_left && (M[r * C::WX] & 1u)) mark(PF16[r * C::WX]);
+                const uint32_t wl = M[r * C::WX + C::WX - 1];
+                if (has_right && (wl >> 31)) {
+                    const uint32_t wll = C::WX > 1 ? M[r * C::WX + C::WX - 2] : 0u;
+                    mark(node_of(PF16[r * C::WX + C::WX - 1], word_starts<RUNS>(wl, wll), 31));
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t nf = FR[0];
+        for (uint32_t k = tid; k < nf; k += C::NT) {
+            const uint32_t x = FR[1 + k];
+            const uint32_t gi = pos_gidx<C>(POS[x], x0, y0, g);
+            wt[C::W_LIST + k] = gi;
+            Lf[gi - g.base] = gi;  // forest registration for kernel (d)
+            POS[x] = uint16_t(kTag | k);
+            FR[1 + k] = gi;
+        }
+        if (tid == 0) {
+            wt[C::W_HEAD + 0] = nf;
+            wt[C::W_HEAD + 1] = nodes;
+        }
+        __syncthreads();
+
+        // ---- node table: local root position, or kTag | rank for seam-touching roots
+        for (uint32_t id = tid; id < nodes; id += C::NT) P[id] = POS[P[id]];
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-            tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(fz), stg);  // OOB clipped
-            tma_store_commit_and_wait();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_store(wt + C::W_MASK, M, C::MW * 6);  // masks + u16 prefixes (contiguous)
+            if (nodes) bulk_store(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+
+        // ---- seam records (every border pixel: its local root's global index
+        // or background) for kernel (d); strip-edge rows also into L for the
+        // strip seam export
+        const uint16_t* T = P;
+        for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
+            int r, c;
+            if (i < C::TW) { r = 0; c = i; }
+            else if (i < 2 * C::TW) { r = C::TH - 1; c = i - C::TW; }
+            else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; }
+            else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; }
+            const int w = c >> 5, b = c & 31;
+            const uint32_t wm = M[r * C::WX + w];
+            uint32_t v = kBG;
+            if ((wm >> b) & 1u) {
+                const uint32_t wl = w > 0 ? M[r * C::WX + w - 1] : 0u;
+                const uint32_t code = T[node_of(PF16[r * C::WX + w], word_starts<RUNS>(wm, wl), uint32_t(b))];
+                if (code & kTag) v = FR[1 + (code & 0x7FFFu)];  // sides facing the image edge are untagged
+            }
+            wt[C::W_REC + i] = v;
+            if (i < 2 * C::TW) {
+                const bool edge = (i < C::TW) ? (ty == 0 && g.edge_above) : (ty + 1 == g.nty && g.edge_below);
+                const uint32_t gy = y0 + r, gx = x0 + c;
+                if (edge && gx < g.W) Lf[size_t(gy) * g.W + gx] = v;
+            }
         }
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ kernel (d)
+// Algorithm 2 over the compact seam records: one warp per 32 pixel pairs of a
+// tile seam (coalesced record loads); a pair whose predecessor along the seam
+// is also foreground on both sides joins the same two local components and is
+// skipped (one union per overlapping run).  Global atomicMin union-find in L.
+template <class C>
+__global__ void __launch_bounds__(256) k_seams(uint32_t* L, const uint32_t* work, Geo g) {
+    constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
+    const uint32_t fz = blockIdx.y;
+    uint32_t* Lf = L + size_t(fz) * g.frame_px;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nh = (g.nty - 1) * g.ntx * HC;
+    const uint32_t nv = (g.ntx - 1) * g.nty * VC;
+    const uint32_t *ra, *rb;
+    uint32_t c;
+    if (gw < nh) {  // horizontal seam: bottom record of (tx, ty) vs top record of (tx, ty + 1)
+        const uint32_t s = gw / HC;
+        c = gw - s * HC;
+        const uint32_t ty = s / g.ntx, tx = s - ty * g.ntx;
+        const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
+        ra = work + ta * C::TILE_WORDS + C::W_REC + C::TW;
+        rb = work + (ta + g.ntx) * C::TILE_WORDS + C::W_REC;
+    } else if (gw < nh + nv) {  // vertical seam: right record of (tx, ty) vs left record of (tx + 1, ty)
+        const uint32_t u = gw - nh, s = u / VC;
+        c = u - s * VC;
+        const uint32_t ty = s / (g.ntx - 1), tx = s - ty * (g.ntx - 1);
+        const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
+        ra = work + ta * C::TILE_WORDS + C::W_REC + 2 * C::TW + C::TH;
+        rb = work + (ta + 1) * C::TILE_WORDS + C::W_REC + 2 * C::TW;
+    } else {
+        return;  // whole warp
+    }
+    const uint32_t i = c * 32 + lane;
+    const uint32_t a = ra[i], b = rb[i];
+    const bool fg = (a != kBG) && (b != kBG);
+    bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
+    if (lane == 0) prev = c > 0 && ra[i - 1] != kBG && rb[i - 1] != kBG;
+    if (fg && !prev) gunion(Lf, g.base, a, b);
+}
+
+// ------------------------------------------------------------------ kernel (d2)
+// After every union (and, in strip mode, after the strip seam resolve): the
+// final label of each tile's seam-touching roots, written over the tile's
+// root list, so kernel (e) needs no forest walks.  One warp per tile.
+template <class C>
+__global__ void __launch_bounds__(256) k_resolve(uint32_t* L, uint32_t* work, Geo g, uint32_t ntiles) {
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    uint32_t* wt = work_tile<C>(work, t);
+    const uint32_t nf = wt[C::W_HEAD];
+    uint32_t* Lf = L + size_t(tile_of(t, g).fz) * g.frame_px;
+    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = gfind(Lf, g.base, wt[C::W_LIST + k]);
+}
+
+// ------------------------------------------------------------------ kernel (e)
+// Persistent, 3-stage pipeline per CTA: while tile i is expanded, the node
+// table + resolved seam labels of tile i+1 and the head/masks of tile i+2 are
+// in flight (bulk copies).  Each warp expands its 32x32 block into a 128B-
+// swizzled staging tile and writes it with one TMA store: every label is
+// written exactly once and the image is never re-read.
+template <class C, bool RUNS, bool TMA_ST>
+__global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+                                                    const uint32_t* work, Geo g, uint32_t ntiles) {
+    using E = ELayout<C, RUNS>;
+    uint8_t* smem = aligned_smem();
+    uint64_t* b1 = reinterpret_cast<uint64_t*>(smem + E::BAR_OFF);
+    uint64_t* b2 = b1 + 3;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wx = warp % C::WX, wy = warp / C::WX;
+    const int row = wy * 32 + lane;
+    const uint32_t G = gridDim.x;
+    auto s1buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S1_OFF + j * E::S1); };
+    auto s2buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S2_OFF + j * E::S2); };
+    auto s1 = [&](uint32_t t, uint32_t j) {
+        mbar_expect_tx(&b1[j], C::S1_BYTES);
+        bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), C::S1_BYTES, &b1[j]);
+    };
+    auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
+        const uint32_t lb = (head[0] * 4 + 15) & ~15u, tb = (head[1] * 2 + 15) & ~15u;
+        const uint32_t* wt = work_tile<C>(const_cast<uint32_t*>(work), t);
+        mbar_expect_tx(&b2[j], lb + tb);
+        if (lb) bulk_load(s2buf(j), wt + C::W_LIST, lb, &b2[j]);
+        if (tb) bulk_load(s2buf(j) + C::MAXF, wt + C::W_TBL, tb, &b2[j]);
+    };
+    if (tid == 0) {
+        if (TMA_ST) prefetch_tmap(&tm_lab);
+        for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
+        for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
+        const uint32_t t0 = blockIdx.x;
+        if (t0 < ntiles) s1(t0, 0);
+        if (t0 + G < ntiles) s1(t0 + G, 1);
+        if (t0 < ntiles) {
+            mbar_wait(&b1[0], 0);
+            s2(t0, 0, s1buf(0));
+        }
+    }
+    __syncthreads();
+
+    uint8_t* stg = smem + E::STG_OFF + warp * 4096;  // 32 x 32 u32, 128B-swizzled
+    uint8_t* myrow = stg + lane * 128;
+    const int sw = lane & 7;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        const uint32_t j1 = it % 3, j2 = it & 1u;
+        if (tid == 0) {
+            if (t + 2 * G < ntiles) s1(t + 2 * G, (it + 2) % 3);
+            if (t + G < ntiles) {
+                const uint32_t jn = (it + 1) % 3;
+                mbar_wait(&b1[jn], ((it + 1) / 3) & 1u);
+                s2(t + G, (it + 1) & 1u, s1buf(jn));
+            }
+        }
+        mbar_wait(&b1[j1], (it / 3) & 1u);
+        mbar_wait(&b2[j2], (it >> 1) & 1u);
+        const uint32_t* M = s1buf(j1) + 4;
+        const uint16_t* PF16 = reinterpret_cast<const uint16_t*>(M + C::MW);
+        const uint32_t* FT = s2buf(j2);
+        const uint16_t* TBL = reinterpret_cast<const uint16_t*>(FT + C::MAXF);
+        const TileId ti = tile_of(t, g);
+        const uint32_t x0 = ti.tx * C::TW, y0 = ti.ty * C::TH;
+
+        const uint32_t m = M[row * C::WX + wx];
+        const uint32_t lm = wx > 0 ? M[row * C::WX + wx - 1] : 0u;
+        const uint32_t st = word_starts<RUNS>(m, lm);
+        const uint32_t pfx = PF16[row * C::WX + wx];
+        auto lab_of = [&](uint32_t v) -> uint32_t {
+            return (v & kTag) ? FT[v & 0x7FFFu] : pos_gidx<C>(v, x0, y0, g);
+        };
+        if (TMA_ST) {  // this warp's previous TMA store must have read the staging tile
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+        }
+        uint32_t cur = ((st & 1u) || !(m & 1u)) ? kBG : lab_of(TBL[pfx - 1]);  // run continuing from the left
+        {
+            const uint16_t* e = TBL + pfx;
+            uint32_t tt = st;
+            while (tt) {
+                const uint32_t b = __ffs(tt) - 1;
+                tt &= tt - 1;
+                *reinterpret_cast<uint32_t*>(myrow + ((((b >> 2) ^ sw) << 4) | ((b & 3) << 2))) = lab_of(*e++);
+            }
+        }
+        uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            uint4* p = reinterpret_cast<uint4*>(myrow + ((c ^ sw) << 4));
+            uint4 v = *p;
+            uint32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = 4 * c + q;
+                cur = ((st >> i) & 1u) ? a[q] : cur;
+                a[q] = ((m >> i) & 1u) ? cur : kBG;
+            }
+            if (TMA_ST) {
+                *p = make_uint4(a[0], a[1], a[2], a[3]);
+            } else {
+                const uint32_t gy = y0 + row;
+                if (gy < g.H) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t gx = x0 + wx * 32 + 4 * c + q;
+                        if (gx < g.W) Lf[size_t(gy) * g.W + gx] = a[q];
+                    }
+                }
+            }
+        }
+        if (TMA_ST) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg);  // OOB clipped
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+        __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
+    }
+    if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ================================================================== host side
+// Persistent grid: every SM filled to the kernel's occupancy (cached per device).
+template <class K>
+static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles, int slot) {
+    static int cache[64][8];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& per = cache[dev & 63][slot];
+    if (per == 0) {
+        int n = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        per = (n > 0 ? n : 1) * (sms > 0 ? sms : 1);
+    }
+    return unsigned(per < int(ntiles) ? per : int(ntiles));
+}
+
+template <class K>
+static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntiles, int slot) {
+    static int cache[64][4];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& per = cache[dev & 63][slot];
+    if (per == 0) {
+        int n = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        per = (n > 0 ? n : 1) * (sms > 0 ? sms : 1);
+    }
+    return unsigned(per < int(ntiles) ? per : int(ntiles));
+}
+
+static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
+
 template <int VAR>
 static cudaError_t launch_local_v(const LaunchArgs& a) {
     using C = TileCfg;
-    const dim3 grid(a.g.ntx, a.g.nty, a.nframes);
+    using A = ALayout<C, (VAR == 0 || VAR == 1)>;
+    const uint32_t nt = tile_count(a);
     if (a.tma_load) {
         auto k = k_local<C, VAR, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        k<<<grid, C::NT, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.work, a.g);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+        k<<<persistent_grid(k, C::NT, A::SMEM, nt, VAR), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
+                                                                                       a.work, a.g, nt);
     } else {
         auto k = k_local<C, VAR, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        k<<<grid, C::NT, C::SMEM, a.stream>>>(a.tm_img, a.img, a.labels, a.work, a.g);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+        k<<<persistent_grid(k, C::NT, A::SMEM, nt, 4 + VAR), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
+                                                                                           a.work, a.g, nt);
     }
     return cudaGetLastError();
 }
@@ -583,33 +739,43 @@ cudaError_t launch_local(const LaunchArgs& a) {
     }
 }
 
-cudaError_t launch_final(const LaunchArgs& a) {
+template <bool RUNS>
+static cudaError_t launch_final_v(const LaunchArgs& a) {
     using C = TileCfg;
-    const dim3 grid(a.g.ntx, a.g.nty, a.nframes);
+    using E = ELayout<C, RUNS>;
+    const uint32_t nt = tile_count(a);
+    k_resolve<C><<<unsigned((uint64_t(nt) * 32 + 255) / 256), 256, 0, a.stream>>>(a.labels, a.work, a.g, nt);
     if (a.tma_store) {
-        auto k = k_final<C, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::E_SMEM);
-        k<<<grid, C::NT, C::E_SMEM, a.stream>>>(a.tm_lab, a.labels, a.work, a.g);
+        auto k = k_final<C, RUNS, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
+        k<<<persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1), C::NT, E::SMEM, a.stream>>>(a.tm_lab, a.labels,
+                                                                                             a.work, a.g, nt);
     } else {
-        auto k = k_final<C, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::E_SMEM);
-        k<<<grid, C::NT, C::E_SMEM, a.stream>>>(a.tm_lab, a.labels, a.work, a.g);
+        auto k = k_final<C, RUNS, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
+        k<<<persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 2 : 3), C::NT, E::SMEM, a.stream>>>(a.tm_lab, a.labels,
+                                                                                             a.work, a.g, nt);
     }
     return cudaGetLastError();
 }
 
+cudaError_t launch_final(const LaunchArgs& a) {
+    return (a.variant == 0 || a.variant == 1) ? launch_final_v<true>(a) : launch_final_v<false>(a);
+}
+
 cudaError_t launch_seams(const LaunchArgs& a) {
-    const uint64_t n = uint64_t(a.g.W) * (a.g.nty - 1) + uint64_t(a.g.H) * (a.g.ntx - 1);
-    if (n == 0) return cudaSuccess;
-    const dim3 grid(unsigned((n + 255) / 256), a.nframes);
-    k_seams<TileCfg><<<grid, 256, 0, a.stream>>>(a.labels, a.g);
+    using C = TileCfg;
+    const uint64_t warps = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
+    if (warps == 0) return cudaSuccess;
+    const dim3 grid(unsigned((warps * 32 + 255) / 256), a.nframes);
+    k_seams<C><<<grid, 256, 0, a.stream>>>(a.labels, a.work, a.g);
     return cudaGetLastError();
 }
 
 size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes) {
     using C = TileCfg;
     const size_t ntiles = size_t((w + C::TW - 1) / C::TW) * ((h + C::TH - 1) / C::TH) * nframes;
-    return ntiles * (size_t(C::MASK_WORDS + C::HDR_WORDS) * 4 + size_t(C::NWARP) * C::TBL_PER_WARP * 2);
+    return ntiles * size_t(C::TILE_WORDS) * 4;
 }
 
 int tile_w() { return TileCfg::TW; }

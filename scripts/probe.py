@@ -11,6 +11,9 @@ import torch  # noqa: E402
 import paper_1712_09789_b200 as ccl  # noqa: E402
 
 
+CHECK = os.environ.get("PROBE_CHECK", "1") == "1"
+
+
 def flush(buf):
     buf.sum()  # read 1 GiB of clean data: evicts (and writes back) everything in L2
 
@@ -28,11 +31,17 @@ def run(name, img_np, variant="c2fl", iters=10):
         _, t = ccl.label_device(img, out, variant=variant, sync=True)
         ts.append(t)
     med = lambda k: sorted(x[k] for x in ts)[len(ts) // 2]
+    ok = ""
+    if CHECK:
+        import numpy as np
+        import oracle
+        ok = " OK" if np.array_equal(out.cpu().numpy(), oracle.sequential_ccl(img_np)) else " MISMATCH"
+
     px = img.numel()
     tot = med("total_ms")
     gbs = px * 5 / (tot * 1e-3) / 1e9
     print(f"{name:28s} {variant:6s} local {med('local_ms')*1e3:7.1f}us merge {med('merge_ms')*1e3:7.1f}us "
-          f"final {med('final_ms')*1e3:7.1f}us total {tot*1e3:7.1f}us  {px/tot/1e6:8.1f} Gpx/s  {gbs:7.0f} GB/s")
+          f"final {med('final_ms')*1e3:7.1f}us total {tot*1e3:7.1f}us  {px/tot/1e6:8.1f} Gpx/s  {gbs:7.0f} GB/s{ok}")
 
 
 def run_batch(n=128):
@@ -65,6 +74,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--all", action="store_true")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--shapes", action="store_true")
     ap.add_argument("--modes", action="store_true")
     a = ap.parse_args()
     print(torch.cuda.get_device_name(), "tile", ccl.tile_shape())
@@ -73,6 +83,13 @@ if __name__ == "__main__":
         run_big()
         raise SystemExit
     run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0))
+    if a.shapes:
+        import numpy as np
+        run("zeros 8192", np.zeros((8192, 8192), np.uint8))
+        run("ones 8192", np.ones((8192, 8192), np.uint8))
+        for d in (0.1, 0.3, 0.9):
+            run(f"random 8192 d{d}", ccl.random_image(8192, 8192, d, 0))
+        run("random 8192 d0.5", ccl.random_image(8192, 8192, 0.5, 0), "rc2fl")
     if a.quick:
         run("spiral 8192", ccl.pattern_image("spiral", 8192, 8192))
         run("random 8192 d0.7", ccl.random_image(8192, 8192, 0.7, 0))
