@@ -13,14 +13,20 @@
 #ifndef CCL_WAVE
 #define CCL_WAVE 0  // barrier between flatten waves in kernel (a)
 #endif
+#ifndef CCL_ULCAP
+#define CCL_ULCAP 128  // union-list entries per warp in kernel (a)
+#endif
+#ifndef CCL_PHASES
+#define CCL_PHASES 0
+#endif
 #ifndef CCL_MINB
-#define CCL_MINB 3  // min resident CTAs of kernel (a) (register cap)
+#define CCL_MINB 5  // min resident CTAs of kernel (a) (register cap)
 #endif
 #ifndef CCL_TILE_WX
-#define CCL_TILE_WX 8
+#define CCL_TILE_WX 4
 #endif
 #ifndef CCL_TILE_WY
-#define CCL_TILE_WY 1
+#define CCL_TILE_WY 2
 #endif
 
 namespace cclk {

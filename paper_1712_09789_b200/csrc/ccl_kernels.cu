@@ -74,8 +74,10 @@ struct ALayout {
     static constexpr int PF16_OFF = M_OFF + C::MW * 4;                     // u16 prefixes (contiguous: one bulk store)
     static constexpr int PF_OFF = PF16_OFF + C::MW * 2;                    // u32 counts / prefixes
     static constexpr int BT_OFF = PF_OFF + C::MW * 4;                      // band totals (+ total)
-    static constexpr int FR_OFF = BT_OFF + 128;                            // [count, root ids -> global idx]
-    static constexpr int IMG_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
+    static constexpr int FR_OFF = BT_OFF + 128;                            // [count, global idx of seam roots]
+    static constexpr int UL_CAP = CCL_ULCAP;                               // union pairs per warp
+    static constexpr int UL_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
+    static constexpr int IMG_OFF = UL_OFF + C::NWARP * UL_CAP * 4;
     static constexpr int BAR_OFF = IMG_OFF + C::PX;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
 };
@@ -94,6 +96,30 @@ struct ELayout {
 };
 
 constexpr uint32_t kTag = 0x8000u;
+
+// Phase timing of kernel (a) (experiment builds with -DCCL_PHASES=1 only):
+// thread 0 accumulates clock64() deltas between consecutive barriers.
+#if CCL_PHASES
+__device__ unsigned long long g_phase_cycles[16];
+#define CCL_PH_INIT() unsigned long long ph_t0 = clock64(), ph_acc[16] = {}
+#define CCL_PH(k)                                         \
+    do {                                                  \
+        if (threadIdx.x == 0) {                           \
+            const unsigned long long t1_ = clock64();     \
+            ph_acc[k] += t1_ - ph_t0;                     \
+            ph_t0 = t1_;                                  \
+        }                                                 \
+    } while (0)
+#define CCL_PH_DONE()                                                              \
+    do {                                                                           \
+        if (threadIdx.x == 0)                                                      \
+            for (int k_ = 0; k_ < 16; ++k_) atomicAdd(&g_phase_cycles[k_], ph_acc[k_]); \
+    } while (0)
+#else
+#define CCL_PH_INIT() (void)0
+#define CCL_PH(k) (void)0
+#define CCL_PH_DONE() (void)0
+#endif
 
 // Node parents are u16; unions are CAS min-unions on the 16-bit entries.
 using node_t = uint16_t;
@@ -121,9 +147,14 @@ __device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b) {
     }
 }
 
+// Dynamic shared memory rounded up to 1024 B (128B-swizzled TMA tiles).  The
+// offset is added to the __shared__ array itself (no integer round trip), so
+// the compiler keeps the shared address space: LDS/STS with 32-bit addresses
+// instead of generic 64-bit LD/ST.
 __device__ __forceinline__ uint8_t* aligned_smem() {
-    extern __shared__ uint8_t smem_raw[];
-    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t off = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    return smem_raw + off;
 }
 
 // Work-buffer view of one tile (tile index tg over frames x tile rows x tile cols).
@@ -259,6 +290,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         if (blockIdx.x < ntiles) issue(blockIdx.x);
     }
 
+    CCL_PH_INIT();
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const TileId ti = tile_of(t, g);
@@ -271,6 +303,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         // last phase must be done with every smem array
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
+        CCL_PH(0);
         for (int i = tid; i < A::MAXN / 32; i += C::NT) FB[i] = 0u;
         if (tid == 0) FR[0] = 0u;
 
@@ -297,6 +330,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             M[row * C::WX + wx] = mm;
         }
         __syncthreads();
+        CCL_PH(1);
         if (TMA && tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x);  // staging buffer is dead
 
         const uint32_t m = M[row * C::WX + wx];
@@ -350,7 +384,33 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 ++id;
             }
         }
+        // refinement pairs (run, upper run) not covered by a coarse link go to
+        // this warp's union list, so the unions are spread over all 32 lanes
+        // instead of serialising on the lanes that own many of them
+        uint32_t U = RUNS ? (os & ~first) : 0u;
+        uint32_t* UL = reinterpret_cast<uint32_t*>(smem + A::UL_OFF) + warp * A::UL_CAP;
+        uint32_t nul;
+        {
+            const uint32_t cu = __popc(U);
+            uint32_t inc = cu;
+#pragma unroll
+            for (int k = 1; k < 32; k <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, k);
+                if (lane >= k) inc += y;
+            }
+            const bool fits = inc <= uint32_t(A::UL_CAP);
+            nul = __reduce_max_sync(0xffffffffu, fits ? inc : 0u);  // entries actually listed
+            if (fits) {  // all of this lane's pairs fit: list them
+                uint32_t* dst = UL + (inc - cu);
+                while (U) {
+                    const uint32_t b = __ffs(U) - 1;
+                    U &= U - 1;
+                    *dst++ = node_of(pfx, st, b) | (node_of(upfx, ust, b) << 16);
+                }
+            }
+        }
         __syncthreads();
+        CCL_PH(2);
 
         // ---- pointer jumping over the coarse forest (balanced over node ids):
         // coarse links form vertical chains; each round halves their length.
@@ -364,15 +424,18 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                     if (pp != p) vP[id] = node_t(pp);
                 }
                 __syncthreads();
+                CCL_PH(3);
             }
         }
 
         // ---- refinement: min-union of the adjacencies the coarse scans did not link
         {
-            uint32_t U;
-            if (RUNS) U = os & ~first;           // remaining (run, upper run) overlaps
-            else U = (VAR == 3) ? o : 0u;        // NC2FL: every vertical pixel pair
-            while (U) {
+            for (uint32_t k = lane; k < nul; k += 32) {
+                const uint32_t pr = UL[k];
+                nunion(P, pr & 0xFFFFu, pr >> 16);
+            }
+            if (!RUNS) U = (VAR == 3) ? o : 0u;  // NC2FL: every vertical pixel pair
+            while (U) {                           // pairs that did not fit in the list
                 const uint32_t b = __ffs(U) - 1;
                 U &= U - 1;
                 nunion(P, node_of(pfx, st, b), node_of(upfx, ust, b));
@@ -390,8 +453,62 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             }
         }
         __syncthreads();
+        CCL_PH(4);
 
-        // ---- unification: flatten in id order (parents always have smaller ids)
+        // ---- seam-touching roots (components reaching a side that faces a
+        // neighbour tile/strip), balanced over all threads: each is marked once
+        // in the FB bitmap; the winner ranks it, registers it in the global
+        // forest and tags its POS entry with kTag | rank.
+        const bool has_top = ty > 0 || g.edge_above;
+        const bool has_bot = ty + 1 < g.nty || g.edge_below;
+        const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
+        {
+            const uint32_t top_n = PF16[C::WX];               // nodes in row 0
+            const uint32_t bot0 = PF16[(C::TH - 1) * C::WX];  // first node of the last row
+            const uint32_t n1 = has_top ? top_n : 0u;
+            const uint32_t n2 = n1 + (has_bot ? nodes - bot0 : 0u);
+            const uint32_t n3 = n2 + (has_left ? uint32_t(C::TH) : 0u);
+            const uint32_t n4 = n3 + (has_right ? uint32_t(C::TH) : 0u);
+            for (uint32_t i = tid; i < n4; i += C::NT) {
+                uint32_t id;
+                if (i < n1) {
+                    id = i;
+                } else if (i < n2) {
+                    id = bot0 + (i - n1);
+                } else if (i < n3) {
+                    const uint32_t r = i - n2;
+                    if (!(M[r * C::WX] & 1u)) continue;
+                    id = PF16[r * C::WX];
+                } else {
+                    const uint32_t r = i - n3;
+                    const uint32_t wl = M[r * C::WX + C::WX - 1];
+                    if (!(wl >> 31)) continue;
+                    const uint32_t wll = C::WX > 1 ? M[r * C::WX + C::WX - 2] : 0u;
+                    id = node_of(PF16[r * C::WX + C::WX - 1], word_starts<RUNS>(wl, wll), 31);
+                }
+                uint32_t x = P[id], p = P[x];
+                while (p != x) {
+                    x = p;
+                    p = P[x];
+                }
+                const uint32_t bit = 1u << (x & 31);
+                if (!(atomicOr(&FB[x >> 5], bit) & bit)) {
+                    const uint32_t k = atomicAdd(FR, 1u);
+                    const uint32_t gi = pos_gidx<C>(POS[x], x0, y0, g);
+                    wt[C::W_LIST + k] = gi;
+                    Lf[gi - g.base] = gi;  // forest registration for kernel (d)
+                    FR[1 + k] = gi;
+                    POS[x] = uint16_t(kTag | k);
+                }
+            }
+        }
+        __syncthreads();
+        CCL_PH(5);
+
+        // ---- unification + node table in one pass: walk each node to its
+        // root (writing the root back: parents always have smaller ids, so
+        // later walks stop early) and store the root's code in POS[id] (root
+        // entries keep their own code; a non-root POS entry is never read again)
         {
             volatile node_t* vP = P;
             for (uint32_t id = tid; id < nodes; id += C::NT) {
@@ -403,73 +520,28 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                         rr = vP[r];
                     }
                     vP[id] = node_t(r);
+                    POS[id] = POS[r];
                 }
             }
         }
-
-        // ---- seam-touching roots (components reaching a side that faces a
-        // neighbour tile/strip): marked once via the FB bitmap and ranked.
-        // Read-only walks: the flatten above may still be running elsewhere.
-        const bool has_top = ty > 0 || g.edge_above;
-        const bool has_bot = ty + 1 < g.nty || g.edge_below;
-        const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
-        auto mark = [&](uint32_t id) {
-            volatile node_t* vP = P;
-            uint32_t x = vP[id], p = vP[x];
-            while (p != x) {
-                x = p;
-                p = vP[x];
-            }
-            const uint32_t bit = 1u << (x & 31);
-            if (!(atomicOr(&FB[x >> 5], bit) & bit)) FR[1 + atomicAdd(FR, 1u)] = x;
-        };
-        {
-            const uint32_t top_n = PF16[C::WX];                 // nodes in row 0
-            const uint32_t bot0 = PF16[(C::TH - 1) * C::WX];    // first node of the last row
-            if (has_top)
-                for (uint32_t id = tid; id < top_n; id += C::NT) mark(id);
-            if (has_bot)
-                for (uint32_t id = bot0 + tid; id < nodes; id += C::NT) mark(id);
-            if (tid < C::TH) {
-                const int r = tid;
-                if (has_left && (M[r * C::WX] & 1u)) mark(PF16[r * C::WX]);
-                const uint32_t wl = M[r * C::WX + C::WX - 1];
-                if (has_right && (wl >> 31)) {
-                    const uint32_t wll = C::WX > 1 ? M[r * C::WX + C::WX - 2] : 0u;
-                    mark(node_of(PF16[r * C::WX + C::WX - 1], word_starts<RUNS>(wl, wll), 31));
-                }
-            }
-        }
-        __syncthreads();
         const uint32_t nf = FR[0];
-        for (uint32_t k = tid; k < nf; k += C::NT) {
-            const uint32_t x = FR[1 + k];
-            const uint32_t gi = pos_gidx<C>(POS[x], x0, y0, g);
-            wt[C::W_LIST + k] = gi;
-            Lf[gi - g.base] = gi;  // forest registration for kernel (d)
-            POS[x] = uint16_t(kTag | k);
-            FR[1 + k] = gi;
-        }
         if (tid == 0) {
             wt[C::W_HEAD + 0] = nf;
             wt[C::W_HEAD + 1] = nodes;
         }
-        __syncthreads();
-
-        // ---- node table: local root position, or kTag | rank for seam-touching roots
-        for (uint32_t id = tid; id < nodes; id += C::NT) P[id] = POS[P[id]];
         fence_proxy_async_smem();
         __syncthreads();
+        CCL_PH(7);
         if (tid == 0) {
             bulk_store(wt + C::W_MASK, M, C::MW * 6);  // masks + u16 prefixes (contiguous)
-            if (nodes) bulk_store(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u);
+            if (nodes) bulk_store(wt + C::W_TBL, POS, (nodes * 2 + 15) & ~15u);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
 
         // ---- seam records (every border pixel: its local root's global index
         // or background) for kernel (d); strip-edge rows also into L for the
         // strip seam export
-        const uint16_t* T = P;
+        const uint16_t* T = POS;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
             int r, c;
             if (i < C::TW) { r = 0; c = i; }
@@ -493,6 +565,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         }
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    CCL_PH_DONE();
 }
 
 // ------------------------------------------------------------------ kernel (d)
@@ -779,6 +852,17 @@ size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes) {
 }
 
 int tile_w() { return TileCfg::TW; }
+#if CCL_PHASES
+extern "C" int ccl_debug_phases(unsigned long long* out16, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * 8);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 int tile_h() { return TileCfg::TH; }
 
 }  // namespace cclk
