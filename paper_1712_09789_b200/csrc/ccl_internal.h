@@ -13,6 +13,9 @@
 #ifndef CCL_WAVE
 #define CCL_WAVE 0  // barrier between flatten waves in kernel (a)
 #endif
+#ifndef CCL_ILP
+#define CCL_ILP 1  // independent pointer walks per thread in kernel (a)'s node passes
+#endif
 #ifndef CCL_ULCAP
 #define CCL_ULCAP 128  // union-list entries per warp in kernel (a)
 #endif
@@ -20,7 +23,7 @@
 #define CCL_PHASES 0
 #endif
 #ifndef CCL_MINB
-#define CCL_MINB 5  // min resident CTAs of kernel (a) (register cap)
+#define CCL_MINB 6  // min resident CTAs of kernel (a) (register cap)
 #endif
 #ifndef CCL_TILE_WX
 #define CCL_TILE_WX 4

@@ -57,7 +57,7 @@ struct Cfg {
     static constexpr int TILE_WORDS = W_TBL + PX / 2;  // table sized for pixel nodes (worst case)
     static constexpr int S1_BYTES = (W_LIST - W_HEAD) * 4;  // head + masks + prefixes: one bulk copy
     static_assert(TW <= 256 && TH <= 256, "TMA box dims are limited to 256");
-    static_assert(PX <= 0x8000, "positions must leave bit 15 free for the seam-root tag");
+    static_assert(PX <= 0x4000, "positions are 14-bit codes (root entries are 0x8000 | code)");
     static_assert(MW % 8 == 0, "16-byte alignment of the work-buffer sections");
 };
 
@@ -67,9 +67,8 @@ using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
 template <class C, bool RUNS>
 struct ALayout {
     static constexpr int MAXN = RUNS ? C::PX / 2 : C::PX;
-    static constexpr int P_OFF = 0;                                        // u16 parents, then the table
-    static constexpr int POS_OFF = P_OFF + MAXN * 2;                       // u16 node position / seam tag
-    static constexpr int FB_OFF = POS_OFF + MAXN * 2;                      // seam-root bitmap
+    static constexpr int P_OFF = 0;                                        // u16 parents / root codes, then the table
+    static constexpr int FB_OFF = P_OFF + MAXN * 2;                        // seam-root bitmap
     static constexpr int M_OFF = FB_OFF + ((MAXN / 32 * 4 + 127) / 128) * 128;  // row-word masks
     static constexpr int PF16_OFF = M_OFF + C::MW * 4;                     // u16 prefixes (contiguous: one bulk store)
     static constexpr int PF_OFF = PF16_OFF + C::MW * 2;                    // u32 counts / prefixes
@@ -95,7 +94,13 @@ struct ELayout {
     static constexpr int SMEM = BAR_OFF + 64 + 1024;
 };
 
-constexpr uint32_t kTag = 0x8000u;
+// Node entries (u16): a non-root holds its parent id (< 0x8000); a root holds
+// its CODE = kRoot | position-in-tile, or kRoot | kSeam | rank once it is
+// known to touch a tile side (rank = index in the tile's seam-root list).
+// The node table handed to kernel (e) is the array of every node's root code.
+constexpr uint32_t kRoot = 0x8000u;
+constexpr uint32_t kSeam = 0x4000u;
+constexpr uint32_t kCode = 0x3FFFu;
 
 // Phase timing of kernel (a) (experiment builds with -DCCL_PHASES=1 only):
 // thread 0 accumulates clock64() deltas between consecutive barriers.
@@ -126,9 +131,9 @@ using node_t = uint16_t;
 __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
     volatile node_t* vP = P;
     uint32_t p = vP[x];
-    while (p != x) {
+    while (!(p & kRoot)) {
         const uint32_t gp = vP[p];
-        if (gp == p) return p;
+        if (gp & kRoot) return p;
         vP[x] = node_t(gp);  // path halving (ancestor only)
         x = gp;
         p = vP[x];
@@ -136,13 +141,15 @@ __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
     return x;
 }
 __device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b) {
+    volatile node_t* vP = P;
     for (;;) {
         a = nfind(P, a);
         b = nfind(P, b);
         if (a == b) return;
         if (a < b) { const uint32_t t = a; a = b; b = t; }
-        if (atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(a),
-                      static_cast<unsigned short>(b)) == a)
+        const uint32_t ca = vP[a];  // a's root code: link a below b unless a got linked meanwhile
+        if ((ca & kRoot) && atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(ca),
+                                      static_cast<unsigned short>(b)) == ca)
             return;
     }
 }
@@ -173,6 +180,21 @@ __device__ __forceinline__ TileId tile_of(uint32_t t, const Geo& g) {
     const uint32_t ty = r / g.ntx;
     return TileId{r - ty * g.ntx, ty, fz};
 }
+// Persistent tile walk t, t + G, t + 2G, ... without a division per step:
+// the stride G is decomposed once into (frames, rows, columns) of tiles.
+struct TileWalk {
+    TileId cur, step;
+    uint32_t ntx, nty;
+    __device__ __forceinline__ TileWalk(uint32_t t0, uint32_t G, const Geo& g)
+        : cur(tile_of(t0, g)), step(tile_of(G, g)), ntx(g.ntx), nty(g.nty) {}
+    __device__ __forceinline__ void advance() {
+        cur.tx += step.tx;
+        cur.ty += step.ty;
+        cur.fz += step.fz;
+        if (cur.tx >= ntx) { cur.tx -= ntx; ++cur.ty; }
+        if (cur.ty >= nty) { cur.ty -= nty; ++cur.fz; }
+    }
+};
 
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
@@ -264,7 +286,6 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     using A = ALayout<C, RUNS>;
     uint8_t* smem = aligned_smem();
     node_t* P = reinterpret_cast<node_t*>(smem + A::P_OFF);
-    uint16_t* POS = reinterpret_cast<uint16_t*>(smem + A::POS_OFF);
     uint32_t* FB = reinterpret_cast<uint32_t*>(smem + A::FB_OFF);
     uint32_t* M = reinterpret_cast<uint32_t*>(smem + A::M_OFF);
     uint16_t* PF16 = reinterpret_cast<uint16_t*>(smem + A::PF16_OFF);
@@ -279,21 +300,21 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     const int row = wy * 32 + lane;
     const int col0 = wx * 32;
 
-    auto issue = [&](uint32_t t) {  // TMA 2-D tile load, OOB -> 0 == background
-        const TileId q = tile_of(t, g);
+    auto issue_at = [&](const TileId& q) {  // TMA 2-D tile load, OOB -> 0 == background
         mbar_expect_tx(bar, C::PX);
         tma_load_3d(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar);
     };
     if (TMA && tid == 0) {
         prefetch_tmap(&tm_img);
         mbar_init(bar, 1);
-        if (blockIdx.x < ntiles) issue(blockIdx.x);
+        if (blockIdx.x < ntiles) issue_at(tile_of(blockIdx.x, g));
     }
 
     CCL_PH_INIT();
     uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const TileId ti = tile_of(t, g);
+    TileWalk walk(blockIdx.x, gridDim.x, g);
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
+        const TileId ti = walk.cur;
         const uint32_t tx = ti.tx, ty = ti.ty;
         const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
         uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;  // strip/frame-local index = global - base
@@ -331,7 +352,11 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         }
         __syncthreads();
         CCL_PH(1);
-        if (TMA && tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x);  // staging buffer is dead
+        if (TMA && tid == 0 && t + gridDim.x < ntiles) {  // staging buffer is dead: prefetch the next tile
+            TileWalk nx = walk;
+            nx.advance();
+            issue_at(nx.cur);
+        }
 
         const uint32_t m = M[row * C::WX + wx];
         const uint32_t lm = wx > 0 ? M[row * C::WX + wx - 1] : 0u;
@@ -379,8 +404,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 } else if (VAR == 2) {
                     if ((um >> b) & 1u) par = node_of(upfx, ust, b);
                 }
-                P[id] = node_t(par);
-                POS[id] = uint16_t(rowpos + b);
+                P[id] = node_t(par == id ? (kRoot | (rowpos + b)) : par);
                 ++id;
             }
         }
@@ -418,10 +442,21 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
 #pragma unroll 1
             for (int j = 0; j < CCL_JUMP; ++j) {
                 volatile node_t* vP = P;
-                for (uint32_t id = tid; id < nodes; id += C::NT) {
-                    const uint32_t p = vP[id];
-                    const uint32_t pp = vP[p];
-                    if (pp != p) vP[id] = node_t(pp);
+                // CCL_ILP independent nodes per thread in flight (latency-bound pass)
+                for (uint32_t base = tid; base < nodes; base += CCL_ILP * C::NT) {
+                    uint32_t p[CCL_ILP], pp[CCL_ILP];
+#pragma unroll
+                    for (int k = 0; k < CCL_ILP; ++k) {
+                        const uint32_t id = base + k * C::NT;
+                        p[k] = id < nodes ? vP[id] : kRoot;
+                    }
+#pragma unroll
+                    for (int k = 0; k < CCL_ILP; ++k) pp[k] = (p[k] & kRoot) ? p[k] : vP[p[k]];
+#pragma unroll
+                    for (int k = 0; k < CCL_ILP; ++k) {
+                        const uint32_t id = base + k * C::NT;
+                        if (id < nodes && !(pp[k] & kRoot)) vP[id] = node_t(pp[k]);
+                    }
                 }
                 __syncthreads();
                 CCL_PH(3);
@@ -458,7 +493,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         // ---- seam-touching roots (components reaching a side that faces a
         // neighbour tile/strip), balanced over all threads: each is marked once
         // in the FB bitmap; the winner ranks it, registers it in the global
-        // forest and tags its POS entry with kTag | rank.
+        // forest and replaces its code by kRoot | kSeam | rank.
         const bool has_top = ty > 0 || g.edge_above;
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
@@ -486,41 +521,37 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                     const uint32_t wll = C::WX > 1 ? M[r * C::WX + C::WX - 2] : 0u;
                     id = node_of(PF16[r * C::WX + C::WX - 1], word_starts<RUNS>(wl, wll), 31);
                 }
-                uint32_t x = P[id], p = P[x];
-                while (p != x) {
+                uint32_t x = id, p = P[id];
+                while (!(p & kRoot)) {
                     x = p;
                     p = P[x];
                 }
                 const uint32_t bit = 1u << (x & 31);
-                if (!(atomicOr(&FB[x >> 5], bit) & bit)) {
+                if (!(atomicOr(&FB[x >> 5], bit) & bit)) {  // the root's entry still holds its position
                     const uint32_t k = atomicAdd(FR, 1u);
-                    const uint32_t gi = pos_gidx<C>(POS[x], x0, y0, g);
+                    const uint32_t gi = pos_gidx<C>(p & kCode, x0, y0, g);
                     wt[C::W_LIST + k] = gi;
                     Lf[gi - g.base] = gi;  // forest registration for kernel (d)
                     FR[1 + k] = gi;
-                    POS[x] = uint16_t(kTag | k);
+                    P[x] = node_t(kRoot | kSeam | k);
                 }
             }
         }
         __syncthreads();
         CCL_PH(5);
 
-        // ---- unification + node table in one pass: walk each node to its
-        // root (writing the root back: parents always have smaller ids, so
-        // later walks stop early) and store the root's code in POS[id] (root
-        // entries keep their own code; a non-root POS entry is never read again)
+        // ---- unification + node table in one pass: every node's entry becomes
+        // its root's code.  A walk stops at the first code it meets, so nodes
+        // already rewritten (parents always have smaller ids) end walks early.
         {
             volatile node_t* vP = P;
             for (uint32_t id = tid; id < nodes; id += C::NT) {
-                uint32_t r = vP[id];
-                if (r != id) {
-                    uint32_t rr = vP[r];
-                    while (rr != r) {
-                        r = rr;
-                        rr = vP[r];
-                    }
-                    vP[id] = node_t(r);
-                    POS[id] = POS[r];
+                uint32_t p = vP[id];
+                if (!(p & kRoot)) {
+                    do {
+                        p = vP[p];
+                    } while (!(p & kRoot));
+                    vP[id] = node_t(p);
                 }
             }
         }
@@ -534,14 +565,14 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         CCL_PH(7);
         if (tid == 0) {
             bulk_store(wt + C::W_MASK, M, C::MW * 6);  // masks + u16 prefixes (contiguous)
-            if (nodes) bulk_store(wt + C::W_TBL, POS, (nodes * 2 + 15) & ~15u);
+            if (nodes) bulk_store(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
 
         // ---- seam records (every border pixel: its local root's global index
         // or background) for kernel (d); strip-edge rows also into L for the
         // strip seam export
-        const uint16_t* T = POS;
+        const uint16_t* T = P;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
             int r, c;
             if (i < C::TW) { r = 0; c = i; }
@@ -554,7 +585,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             if ((wm >> b) & 1u) {
                 const uint32_t wl = w > 0 ? M[r * C::WX + w - 1] : 0u;
                 const uint32_t code = T[node_of(PF16[r * C::WX + w], word_starts<RUNS>(wm, wl), uint32_t(b))];
-                if (code & kTag) v = FR[1 + (code & 0x7FFFu)];  // sides facing the image edge are untagged
+                if (code & kSeam) v = FR[1 + (code & kCode)];  // sides facing the image edge are not seams
             }
             wt[C::W_REC + i] = v;
             if (i < 2 * C::TW) {
@@ -615,13 +646,40 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* L, const uint32_t* work
 // root list, so kernel (e) needs no forest walks.  One warp per tile.
 template <class C>
 __global__ void __launch_bounds__(256) k_resolve(uint32_t* L, uint32_t* work, Geo g, uint32_t ntiles) {
+    constexpr int K = 4;  // independent forest walks per thread in flight (pure latency chains)
     const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= ntiles) return;
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
-    uint32_t* Lf = L + size_t(tile_of(t, g).fz) * g.frame_px;
-    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = gfind(Lf, g.base, wt[C::W_LIST + k]);
+    const uint32_t* Lf = L + size_t(tile_of(t, g).fz) * g.frame_px;
+    for (uint32_t k0 = lane; k0 < nf; k0 += 32 * K) {
+        uint32_t x[K], p[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const uint32_t k = k0 + 32 * j;
+            x[j] = k < nf ? wt[C::W_LIST + k] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) p[j] = (k0 + 32 * j < nf) ? gload(Lf + (x[j] - g.base)) : x[j];
+        for (;;) {  // read-only walks in lockstep: a parent below base is a foreign terminal root
+            bool more = false;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                if (p[j] != x[j] && p[j] >= g.base) {
+                    x[j] = p[j];
+                    p[j] = gload(Lf + (x[j] - g.base));
+                    more = true;
+                }
+            }
+            if (!more) break;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const uint32_t k = k0 + 32 * j;
+            if (k < nf) wt[C::W_LIST + k] = p[j];
+        }
+    }
 }
 
 // ------------------------------------------------------------------ kernel (e)
@@ -672,7 +730,8 @@ __global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUte
     uint8_t* myrow = stg + lane * 128;
     const int sw = lane & 7;
     uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+    TileWalk walk(blockIdx.x, G, g);
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it, walk.advance()) {
         const uint32_t j1 = it % 3, j2 = it & 1u;
         if (tid == 0) {
             if (t + 2 * G < ntiles) s1(t + 2 * G, (it + 2) % 3);
@@ -688,7 +747,7 @@ __global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUte
         const uint16_t* PF16 = reinterpret_cast<const uint16_t*>(M + C::MW);
         const uint32_t* FT = s2buf(j2);
         const uint16_t* TBL = reinterpret_cast<const uint16_t*>(FT + C::MAXF);
-        const TileId ti = tile_of(t, g);
+        const TileId ti = walk.cur;
         const uint32_t x0 = ti.tx * C::TW, y0 = ti.ty * C::TH;
 
         const uint32_t m = M[row * C::WX + wx];
@@ -696,7 +755,7 @@ __global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUte
         const uint32_t st = word_starts<RUNS>(m, lm);
         const uint32_t pfx = PF16[row * C::WX + wx];
         auto lab_of = [&](uint32_t v) -> uint32_t {
-            return (v & kTag) ? FT[v & 0x7FFFu] : pos_gidx<C>(v, x0, y0, g);
+            return (v & kSeam) ? FT[v & kCode] : pos_gidx<C>(v & kCode, x0, y0, g);
         };
         if (TMA_ST) {  // this warp's previous TMA store must have read the staging tile
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

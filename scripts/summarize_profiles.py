@@ -20,9 +20,10 @@ def launches(path):
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[start]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.OrderedDict()
     for r in rows[start + 1:]:
-        if len(r) < len(h):
+        if len(r) < len(h) or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         agg.setdefault(r[ki], []).append(float(r[vi].replace(",", "")) / 1e3)  # ns -> us
     return agg
@@ -41,7 +42,7 @@ def raw(rep):
 
 
 def short(name):
-    for k in ("k_local", "k_seams", "k_final"):
+    for k in ("k_local_wf", "k_local", "k_seams", "k_resolve", "k_final"):
         if k in name:
             return k
     return name.split("(")[0][-50:]
@@ -62,7 +63,7 @@ def main():
              "shares, not absolutes); traffic/occupancy from one `ncu --set full` capture per kernel.", "",
              "## Launch list (our kernels, mean per launch)", "", "| kernel | launches | mean us | share of step |",
              "|---|---|---|---|"]
-    ours = {short(k): v for k, v in L.items() if "cclk" in k}
+    ours = {short(k): v for k, v in L.items() if short(k).startswith("k_")}
     tot = sum(sum(v) / len(v) for v in ours.values())
     for k, v in ours.items():
         m = sum(v) / len(v)
@@ -73,7 +74,7 @@ def main():
     traffic = {}
     for d, un in R:
         k = short(d["Kernel Name"])
-        if k not in ("k_local", "k_seams", "k_final"):
+        if k not in ("k_local_wf", "k_local", "k_seams", "k_resolve", "k_final"):
             continue
         dur = float(d["gpu__time_duration.sum"].replace(",", ""))
         if un["gpu__time_duration.sum"] == "ms":
@@ -86,7 +87,8 @@ def main():
         smem = d.get("launch__shared_mem_per_block_dynamic", "")
         lines.append(f"| {k} | {dur:.1f} | {rd:.1f} | {wr:.1f} | {(rd + wr) * 1e6 / PX:.2f} | "
                      f"{(rd + wr) * 1e6 / (dur * 1e-6) / 1e9:.0f} | {occ} | {ipc} | {regs} | {smem} |")
-        traffic[{"k_local": "local_ms", "k_seams": "merge_ms", "k_final": "final_ms"}[k]] = (rd + wr) * 1e6
+        key = {"k_local_wf": "local_ms", "k_local": "local_ms", "k_seams": "merge_ms", "k_resolve": "final_ms", "k_final": "final_ms"}[k]
+        traffic[key] = traffic.get(key, 0.0) + (rd + wr) * 1e6  # final_ms spans (d2) resolve + (e)
     os.makedirs(os.path.join(REPO, "profiles"), exist_ok=True)
     with open(os.path.join(REPO, "profiles", f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
