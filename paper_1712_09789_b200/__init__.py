@@ -75,8 +75,8 @@ _sig("ccl_label_device", _c, _vp, _vp, _sz, _u32, _u32, _vp, _c, _vp, _c, ctypes
 _sig("ccl_label_host", _c, _vp, _u8p, _u32, _u32, _u32p, _c, ctypes.POINTER(ctypes.c_float))
 _sig("ccl_label_batch", _c, _vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _c, _vp)
 _sig("ccl_strip_local", _c, _vp, _vp, _sz, _u32, _u32, _u32, _u32, _vp, _vp, _c, _vp)
-_sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
-_sig("ccl_strip_seam_resolve", _c, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
+_sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
+_sig("ccl_strip_seam_resolve", _c, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
 _sig("ccl_strip_final", _c, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
 _sig("ccl_strip_scratch_words", _sz, _u32, _u32)
 _sig("ccl_work_bytes", _sz, _u32, _u32, _u32)

@@ -6,11 +6,12 @@
 //   export  : k_strip_roots -> k_strip_repmin -> k_strip_reps
 //   exchange: all-gather of every strip's 4*W seam words (caller: NCCL)
 //   resolve : k_seam_union (identical on every strip) -> k_seam_apply
-// k_seam_apply writes, for each of this strip's seam roots r, the final label
-// f <= r into the strip's forest entry L[r - base].  f may belong to another
-// strip (f < base): gfind treats such a value as a terminal root, so kernel
-// (e) needs no separate remap table.
-//
+// Kernel (a) leaves, in the strip area of the work buffer, the compact forest
+// node of every top/bottom-row pixel; k_strip_roots resolves them to the
+// strip-local roots (exported by key = global raster index) and remembers the
+// compact root per column, and k_seam_apply overwrites that root's key with
+// the component's final label f <= key (possibly another strip's pixel), which
+// kernel (d2) then hands to kernel (e) like any other root label.
 // Compaction (pipeline.cpp:54-70): compacted label =
 // 1 + rank of the component root among all roots (roots are component minima,
 // so raster order of first appearance == ascending root order).
@@ -23,24 +24,26 @@
 namespace cclk {
 
 // ------------------------------------------------------------ strip export
-__global__ void k_strip_roots(uint32_t* L, Geo g, uint32_t* out) {
+__global__ void k_strip_roots(const uint32_t* se, Forest fst, uint32_t* L, Geo g, uint32_t* out, uint32_t* croot) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * g.W) return;
     const bool top = i < g.W;
-    const uint32_t x = top ? i : i - g.W;
-    uint32_t r = kBG;
+    uint32_t r = kBG, cr = kBG;
     if (top ? g.edge_above : g.edge_below) {
-        const uint32_t row = top ? 0u : g.H - 1;
-        const uint32_t v = L[size_t(row) * g.W + x];  // seam pixel: its tile-local root (kernel a)
-        if (v != kBG) r = gfind(L, g.base, v);        // strip-local root after kernel (d)
+        const uint32_t v = se[i];  // compact node of the edge pixel's tile-local root
+        if (v != kBG) {
+            cr = fst.find(v);      // strip-local root after kernel (d)
+            r = fst.key(cr);
+            L[r - g.base] = r;     // scratch for k_strip_repmin (L is rewritten by kernel (e))
+        }
     }
     out[i] = r;
+    croot[i] = cr;
 }
 
 // Bottom-row roots that are not on the top row: the first (min x) bottom node
-// carrying the root is found with an atomicMin on the root's own forest entry,
-// encoded as base + x (< base + W <= root, so the root value itself loses).
-// The entry is restored by k_seam_apply, which rewrites every seam root.
+// carrying the root is found with an atomicMin on the root's scratch entry in
+// L, encoded as base + x (< base + W <= root, so the root value itself loses).
 __global__ void k_strip_repmin(uint32_t* L, Geo g, const uint32_t* out) {
     const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= g.W) return;
@@ -105,7 +108,8 @@ __global__ void k_seam_union(const uint32_t* all, uint32_t N, uint32_t W, uint32
         if (atomicCAS(par + b, b, a) == b) return;  // link larger-key root below smaller-key root
     }
 }
-__global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const uint32_t* par, uint32_t* L, Geo g) {
+__global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const uint32_t* par, const uint32_t* croot,
+                             Forest fst) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * W) return;
     const uint32_t j = k * 2 * W + i;
@@ -113,19 +117,22 @@ __global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const 
     if (r == kBG) return;
     uint32_t q = j;
     while (par[q] != q) q = par[q];
-    L[r - g.base] = seam_key(all, W, q);
+    fst.f[2 * size_t(croot[i]) + 1] = seam_key(all, W, q);  // final label of this strip root
 }
 
-cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* seam_out, uint32_t k, cudaStream_t s) {
+cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* work, uint32_t* seam_out, uint32_t k,
+                                cudaStream_t s) {
     const unsigned nb2 = (2 * g.W + 255) / 256, nb1 = (g.W + 255) / 256;
-    k_strip_roots<<<nb2, 256, 0, s>>>(labels, g, seam_out);
+    uint32_t* se = strip_area_ptr(work, g);
+    k_strip_roots<<<nb2, 256, 0, s>>>(se, Forest{forest_ptr(work, g)}, labels, g, seam_out, se + 2 * size_t(g.W));
     k_strip_repmin<<<nb1, 256, 0, s>>>(labels, g, seam_out);
     k_strip_reps<<<nb2, 256, 0, s>>>(labels, g, k, seam_out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* all, uint32_t N, uint32_t k, uint32_t* labels,
-                                 uint32_t* scratch, cudaStream_t s) {
+                                 uint32_t* work, uint32_t* scratch, cudaStream_t s) {
+    (void)labels;
     const size_t W = g.W;
     cudaError_t e = cudaMemcpy2DAsync(scratch, 2 * W * 4, all + 2 * W, 4 * W * 4, 2 * W * 4, N,
                                       cudaMemcpyDeviceToDevice, s);
@@ -134,7 +141,8 @@ cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* all, uint32_t N, 
         const uint64_t n = uint64_t(N - 1) * W;
         k_seam_union<<<unsigned((n + 255) / 256), 256, 0, s>>>(all, N, g.W, scratch);
     }
-    k_seam_apply<<<unsigned((2 * W + 255) / 256), 256, 0, s>>>(all, g.W, k, scratch, labels, g);
+    k_seam_apply<<<unsigned((2 * W + 255) / 256), 256, 0, s>>>(all, g.W, k, scratch,
+                                                              strip_area_ptr(work, g) + 2 * W, Forest{forest_ptr(work, g)});
     return cudaGetLastError();
 }
 

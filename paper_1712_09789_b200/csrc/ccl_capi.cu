@@ -318,27 +318,29 @@ ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch,
 }
 
 ccl_status ccl_strip_seam_export(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
-                                 uint32_t strip_index, uint32_t* d_labels, uint32_t* d_seam_out, void* stream) {
-    if (!ctx || !d_labels || !d_seam_out) return fail(CCL_EINVAL, "null argument");
+                                 uint32_t strip_index, uint32_t* d_labels, void* d_work, uint32_t* d_seam_out,
+                                 void* stream) {
+    if (!ctx || !d_labels || !d_work || !d_seam_out) return fail(CCL_EINVAL, "null argument");
     DeviceGuard dg(ctx->device);
     cclk::Geo g{};
     if (ccl_status s = strip_geo(w, h, row0, full_h, w, &g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CCL_CHECK(cclk::launch_strip_export(g, d_labels, d_seam_out, strip_index, st));
+    CCL_CHECK(cclk::launch_strip_export(g, d_labels, static_cast<uint32_t*>(d_work), d_seam_out, strip_index, st));
     return CCL_OK;
 }
 
 ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint32_t n_strips, uint32_t strip_index,
                                   uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, uint32_t* d_labels,
-                                  uint32_t* d_scratch, void* stream) {
-    if (!ctx || !d_seam_all || !d_labels || !d_scratch) return fail(CCL_EINVAL, "null argument");
+                                  void* d_work, uint32_t* d_scratch, void* stream) {
+    if (!ctx || !d_seam_all || !d_labels || !d_work || !d_scratch) return fail(CCL_EINVAL, "null argument");
     if (n_strips == 0 || strip_index >= n_strips) return fail(CCL_EINVAL, "bad strip index");
     if (uint64_t(n_strips) * 2 * w >= 0xFFFFFFFFull) return fail(CCL_EINVAL, "too many seam nodes");
     DeviceGuard dg(ctx->device);
     cclk::Geo g{};
     if (ccl_status s = strip_geo(w, h, row0, full_h, w, &g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CCL_CHECK(cclk::launch_strip_resolve(g, d_seam_all, n_strips, strip_index, d_labels, d_scratch, st));
+    CCL_CHECK(cclk::launch_strip_resolve(g, d_seam_all, n_strips, strip_index, d_labels,
+                                         static_cast<uint32_t*>(d_work), d_scratch, st));
     return CCL_OK;
 }
 

@@ -71,50 +71,43 @@ __device__ __forceinline__ void sunion(uint32_t* P, uint32_t a, uint32_t b) {
 }
 
 // --------------------------------------------------------- global union-find
-// The forest lives in the output label buffer L itself (no extra W*H array).
-// Node ids are global raster indices; `base` is the first index held by this
-// buffer (strip mode) — a parent value < base is a foreign, terminal root
-// written by the strip seam resolve.
 __device__ __forceinline__ uint32_t gload(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ uint32_t gfind(uint32_t* L, uint32_t base, uint32_t x) {
-    uint32_t p = gload(L + (x - base));
-    while (p != x) {
-        if (p < base) return p;
-        const uint32_t gp = gload(L + (p - base));
-        if (gp == p || gp < base) return gp;
-        L[x - base] = gp;  // path halving
-        x = gp;
-        p = gload(L + (x - base));
-    }
-    return x;
-}
-// Read-only variant for the final relabel: kernel (e) overwrites every
-// pixel's entry with its final label while other CTAs still walk the forest,
-// so a halving store could land after (and clobber) a final label.
-__device__ __forceinline__ uint32_t gfind_ro(const uint32_t* L, uint32_t base, uint32_t x) {
-    uint32_t p = gload(L + (x - base));
-    while (p != x && p >= base) {
-        x = p;
-        p = gload(L + (x - base));
-    }
-    return p;
-}
-__device__ __forceinline__ void gunion(uint32_t* L, uint32_t base, uint32_t a, uint32_t b) {
-    for (;;) {
-        a = gfind(L, base, a);
-        b = gfind(L, base, b);
-        if (a == b) return;
-        if (a < b) { const uint32_t t = a; a = b; b = t; }
-        const uint32_t old = atomicMin(L + (a - base), b);
-        if (old == a) return;
-        a = old;
-    }
-}
 
+// Compact global forest (kernels (a) register, (d) unions, (d2) resolves).
+// Parents are node ids; the class root is the node with the smallest key, so
+// its key is the component's minimum raster index (forest.hpp:98-111 min-union
+// semantics, restated over seam-touching roots only).  ~10 MB touched at 8192^2:
+// the walks hit L2 instead of scattered HBM sectors of the label buffer.
+struct Forest {
+    uint32_t* f;  // f[2n] = parent, f[2n+1] = key
+    __device__ __forceinline__ uint32_t parent(uint32_t n) const { return gload(f + 2 * size_t(n)); }
+    __device__ __forceinline__ uint32_t key(uint32_t n) const { return gload(f + 2 * size_t(n) + 1); }
+    __device__ __forceinline__ uint32_t find(uint32_t x) const {
+        uint32_t p = parent(x);
+        while (p != x) {
+            const uint32_t gp = parent(p);
+            if (gp == p) return p;
+            f[2 * size_t(x)] = gp;  // path halving (ancestor only)
+            x = gp;
+            p = parent(x);
+        }
+        return x;
+    }
+    __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
+        for (;;) {
+            a = find(a);
+            b = find(b);
+            if (a == b) return;
+            const uint32_t ka = key(a), kb = key(b);
+            if (ka < kb) { const uint32_t t = a; a = b; b = t; }  // a: the larger key
+            if (atomicCAS(f + 2 * size_t(a), a, b) == a) return;
+        }
+    }
+};
 // --------------------------------------------------------------- TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

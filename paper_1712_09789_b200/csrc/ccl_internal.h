@@ -65,14 +65,17 @@ cudaError_t launch_seams(const LaunchArgs& a);
 cudaError_t launch_final(const LaunchArgs& a);
 
 // strip-mode and compaction kernels (ccl_aux.cu)
-cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* seam_out, uint32_t strip_index,
-                                cudaStream_t s);
+cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* work, uint32_t* seam_out,
+                                uint32_t strip_index, cudaStream_t s);
 cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* seam_all, uint32_t n_strips, uint32_t strip_index,
-                                 uint32_t* labels, uint32_t* scratch, cudaStream_t s);
+                                 uint32_t* labels, uint32_t* work, uint32_t* scratch, cudaStream_t s);
 cudaError_t launch_compact(const uint32_t* raw, size_t n, uint32_t* out, uint32_t* scratch, cudaStream_t s);
 size_t compact_scratch_words(size_t n);
 
 size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
+uint32_t* strip_area_ptr(uint32_t* work, const Geo& g);  // strip mode: [edge nodes 2W | edge roots 2W]
+uint32_t* forest_ptr(uint32_t* work, const Geo& g);      // compact global forest
+int tile_maxf();
 int tile_w();
 int tile_h();
 

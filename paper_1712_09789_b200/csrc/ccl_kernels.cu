@@ -56,6 +56,9 @@ struct Cfg {
     static constexpr int W_TBL = W_REC + 2 * TW + 2 * TH;
     static constexpr int TILE_WORDS = W_TBL + PX / 2;  // table sized for pixel nodes (worst case)
     static constexpr int S1_BYTES = (W_LIST - W_HEAD) * 4;  // head + masks + prefixes: one bulk copy
+    // After the tiles: the COMPACT global forest, one {parent, key} u32 pair per
+    // possible seam-touching root (node n = tile * MAXF + rank, key = the root's
+    // global raster index), then the strip-mode area (edge rows + their roots).
     static_assert(TW <= 256 && TH <= 256, "TMA box dims are limited to 256");
     static_assert(PX <= 0x4000, "positions are 14-bit codes (root entries are 0x8000 | code)");
     static_assert(MW % 8 == 0, "16-byte alignment of the work-buffer sections");
@@ -168,6 +171,15 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
 template <class C>
 __device__ __forceinline__ uint32_t* work_tile(uint32_t* work, size_t tg) {
     return work + tg * size_t(C::TILE_WORDS);
+}
+
+template <class C>
+__device__ __forceinline__ Forest forest_of(uint32_t* work, uint32_t ntiles) {
+    return Forest{work + size_t(ntiles) * C::TILE_WORDS};
+}
+template <class C>
+__device__ __forceinline__ uint32_t* strip_area(uint32_t* work, uint32_t ntiles) {
+    return work + size_t(ntiles) * C::TILE_WORDS + 2 * size_t(ntiles) * C::MAXF;
 }
 
 // Linear tile index -> (tx, ty, frame).
@@ -299,6 +311,8 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane;
     const int col0 = wx * 32;
+    const Forest fst = forest_of<C>(work, ntiles);
+    uint32_t* SE = strip_area<C>(work, ntiles);  // strip mode: edge-row nodes [top W | bottom W]
 
     auto issue_at = [&](const TileId& q) {  // TMA 2-D tile load, OOB -> 0 == background
         mbar_expect_tx(bar, C::PX);
@@ -317,7 +331,6 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         const TileId ti = walk.cur;
         const uint32_t tx = ti.tx, ty = ti.ty;
         const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
-        uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;  // strip/frame-local index = global - base
         uint32_t* wt = work_tile<C>(work, t);
 
         // the previous tile's bulk stores must have read P / M / PF16, and its
@@ -529,10 +542,10 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 const uint32_t bit = 1u << (x & 31);
                 if (!(atomicOr(&FB[x >> 5], bit) & bit)) {  // the root's entry still holds its position
                     const uint32_t k = atomicAdd(FR, 1u);
-                    const uint32_t gi = pos_gidx<C>(p & kCode, x0, y0, g);
-                    wt[C::W_LIST + k] = gi;
-                    Lf[gi - g.base] = gi;  // forest registration for kernel (d)
-                    FR[1 + k] = gi;
+                    const uint32_t n = t * uint32_t(C::MAXF) + k;  // compact global node
+                    fst.f[2 * size_t(n)] = n;
+                    fst.f[2 * size_t(n) + 1] = pos_gidx<C>(p & kCode, x0, y0, g);
+                    FR[1 + k] = n;
                     P[x] = node_t(kRoot | kSeam | k);
                 }
             }
@@ -569,9 +582,9 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
 
-        // ---- seam records (every border pixel: its local root's global index
-        // or background) for kernel (d); strip-edge rows also into L for the
-        // strip seam export
+        // ---- seam records (every border pixel: its root's compact global node
+        // or background) for kernel (d); strip-edge rows also into the strip
+        // area for the strip seam export
         const uint16_t* T = P;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
             int r, c;
@@ -589,9 +602,10 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             }
             wt[C::W_REC + i] = v;
             if (i < 2 * C::TW) {
-                const bool edge = (i < C::TW) ? (ty == 0 && g.edge_above) : (ty + 1 == g.nty && g.edge_below);
-                const uint32_t gy = y0 + r, gx = x0 + c;
-                if (edge && gx < g.W) Lf[size_t(gy) * g.W + gx] = v;
+                const bool top = i < C::TW;
+                const bool edge = top ? (ty == 0 && g.edge_above) : (ty + 1 == g.nty && g.edge_below);
+                const uint32_t gx = x0 + c;
+                if (edge && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
             }
         }
     }
@@ -605,10 +619,10 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
 // is also foreground on both sides joins the same two local components and is
 // skipped (one union per overlapping run).  Global atomicMin union-find in L.
 template <class C>
-__global__ void __launch_bounds__(256) k_seams(uint32_t* L, const uint32_t* work, Geo g) {
+__global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t ntiles) {
     constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
     const uint32_t fz = blockIdx.y;
-    uint32_t* Lf = L + size_t(fz) * g.frame_px;
+    const Forest fst = forest_of<C>(work, ntiles);
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t nh = (g.nty - 1) * g.ntx * HC;
@@ -637,7 +651,7 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* L, const uint32_t* work
     const bool fg = (a != kBG) && (b != kBG);
     bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
     if (lane == 0) prev = c > 0 && ra[i - 1] != kBG && rb[i - 1] != kBG;
-    if (fg && !prev) gunion(Lf, g.base, a, b);
+    if (fg && !prev) fst.unite(a, b);
 }
 
 // ------------------------------------------------------------------ kernel (d2)
@@ -645,41 +659,14 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* L, const uint32_t* work
 // final label of each tile's seam-touching roots, written over the tile's
 // root list, so kernel (e) needs no forest walks.  One warp per tile.
 template <class C>
-__global__ void __launch_bounds__(256) k_resolve(uint32_t* L, uint32_t* work, Geo g, uint32_t ntiles) {
-    constexpr int K = 4;  // independent forest walks per thread in flight (pure latency chains)
+__global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t ntiles) {
     const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= ntiles) return;
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
-    const uint32_t* Lf = L + size_t(tile_of(t, g).fz) * g.frame_px;
-    for (uint32_t k0 = lane; k0 < nf; k0 += 32 * K) {
-        uint32_t x[K], p[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const uint32_t k = k0 + 32 * j;
-            x[j] = k < nf ? wt[C::W_LIST + k] : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < K; ++j) p[j] = (k0 + 32 * j < nf) ? gload(Lf + (x[j] - g.base)) : x[j];
-        for (;;) {  // read-only walks in lockstep: a parent below base is a foreign terminal root
-            bool more = false;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                if (p[j] != x[j] && p[j] >= g.base) {
-                    x[j] = p[j];
-                    p[j] = gload(Lf + (x[j] - g.base));
-                    more = true;
-                }
-            }
-            if (!more) break;
-        }
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const uint32_t k = k0 + 32 * j;
-            if (k < nf) wt[C::W_LIST + k] = p[j];
-        }
-    }
+    const Forest fst = forest_of<C>(work, ntiles);
+    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.key(fst.find(t * uint32_t(C::MAXF) + k));
 }
 
 // ------------------------------------------------------------------ kernel (e)
@@ -876,7 +863,7 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
     using C = TileCfg;
     using E = ELayout<C, RUNS>;
     const uint32_t nt = tile_count(a);
-    k_resolve<C><<<unsigned((uint64_t(nt) * 32 + 255) / 256), 256, 0, a.stream>>>(a.labels, a.work, a.g, nt);
+    k_resolve<C><<<unsigned((uint64_t(nt) * 32 + 255) / 256), 256, 0, a.stream>>>(a.work, a.g, nt);
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
@@ -900,15 +887,25 @@ cudaError_t launch_seams(const LaunchArgs& a) {
     const uint64_t warps = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
     if (warps == 0) return cudaSuccess;
     const dim3 grid(unsigned((warps * 32 + 255) / 256), a.nframes);
-    k_seams<C><<<grid, 256, 0, a.stream>>>(a.labels, a.work, a.g);
+    k_seams<C><<<grid, 256, 0, a.stream>>>(a.work, a.g, tile_count(a));
     return cudaGetLastError();
 }
 
 size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes) {
     using C = TileCfg;
     const size_t ntiles = size_t((w + C::TW - 1) / C::TW) * ((h + C::TH - 1) / C::TH) * nframes;
-    return ntiles * size_t(C::TILE_WORDS) * 4;
+    return (ntiles * (size_t(C::TILE_WORDS) + 2 * size_t(C::MAXF)) + 4 * size_t(w)) * 4;
 }
+
+uint32_t* strip_area_ptr(uint32_t* work, const Geo& g) {
+    using C = TileCfg;
+    return work + size_t(g.ntx) * g.nty * (size_t(C::TILE_WORDS) + 2 * size_t(C::MAXF));
+}
+uint32_t* forest_ptr(uint32_t* work, const Geo& g) {
+    using C = TileCfg;
+    return work + size_t(g.ntx) * g.nty * size_t(C::TILE_WORDS);
+}
+int tile_maxf() { return TileCfg::MAXF; }
 
 int tile_w() { return TileCfg::TW; }
 #if CCL_PHASES

@@ -67,14 +67,15 @@ class StripLabeler:
         _check(_lib.ccl_strip_local(c, img.data_ptr(), img.stride(0), self.w, self.h, self.row0, self.full_h,
                                     out.data_ptr(), self.work.data_ptr(), v, s))
         _check(_lib.ccl_strip_seam_export(c, self.w, self.h, self.row0, self.full_h, self.rank, out.data_ptr(),
-                                          self.seam.data_ptr(), s))
+                                          self.work.data_ptr(), self.seam.data_ptr(), s))
         if stream is not None:
             with torch.cuda.stream(stream):
                 allseams = exchange_seams(self.seam, self.world, self.group)
         else:
             allseams = exchange_seams(self.seam, self.world, self.group)
         _check(_lib.ccl_strip_seam_resolve(c, allseams.data_ptr(), self.world, self.rank, self.w, self.h, self.row0,
-                                           self.full_h, out.data_ptr(), self.scratch.data_ptr(), s))
+                                           self.full_h, out.data_ptr(), self.work.data_ptr(), self.scratch.data_ptr(),
+                                           s))
         _check(_lib.ccl_strip_final(c, self.w, self.h, self.row0, self.full_h, out.data_ptr(), self.work.data_ptr(),
                                     s))
         return out
@@ -102,10 +103,11 @@ def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx
         views.append((im, lo, r0, h, wk))
         _check(_lib.ccl_strip_local(ctx.handle, im.data_ptr(), im.stride(0), w, h, r0, h_full, lo.data_ptr(),
                                     wk.data_ptr(), v, s))
-        _check(_lib.ccl_strip_seam_export(ctx.handle, w, h, r0, h_full, k, lo.data_ptr(), seams[k].data_ptr(), s))
+        _check(_lib.ccl_strip_seam_export(ctx.handle, w, h, r0, h_full, k, lo.data_ptr(), wk.data_ptr(),
+                                          seams[k].data_ptr(), s))
     for k, (im, lo, r0, h, wk) in enumerate(views):
         _check(_lib.ccl_strip_seam_resolve(ctx.handle, seams.data_ptr(), n_strips, k, w, h, r0, h_full, lo.data_ptr(),
-                                           scratch.data_ptr(), s))
+                                           wk.data_ptr(), scratch.data_ptr(), s))
     for k, (im, lo, r0, h, wk) in enumerate(views):
         _check(_lib.ccl_strip_final(ctx.handle, w, h, r0, h_full, lo.data_ptr(), wk.data_ptr(), s))
     return out

@@ -97,7 +97,7 @@ def test_host_compact_matches_oracle(ccl, oracle_mod, small_cases):
 def test_strip_split(ccl):
     from paper_1712_09789_b200.strips import split_rows
     th = ccl.tile_shape()[1]
-    for full_h, n in [(8192 * 8, 8), (1080, 3), (1000, 4), (33, 1), (64, 2)]:
+    for full_h, n in [(8192 * 8, 8), (1080, 3), (1000, 4), (33, 1), (2 * th, 2)]:
         parts = split_rows(full_h, n)
         assert sum(h for _, h in parts) == full_h and len(parts) == n
         assert all(h % th == 0 for _, h in parts[:-1])

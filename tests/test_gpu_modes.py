@@ -55,7 +55,8 @@ def test_virtual_strips(ccl, oracle_mod, kind, n):
 def test_virtual_strips_odd_width(ccl, oracle_mod):
     import torch
     from paper_1712_09789_b200.strips import label_strips_single_gpu
-    for (w, h, n) in [(97, 200, 3), (1, 640, 5), (300, 64, 2), (1003, 300, 4)]:
+    th = ccl.tile_shape()[1]
+    for (w, h, n) in [(97, 3 * th + 8, 3), (1, 10 * th, 5), (300, 2 * th, 2), (1003, 300, 4)]:
         img = ccl.random_image(w, h, 0.6, w + h)
         got = label_strips_single_gpu(torch.from_numpy(img).cuda(), n).cpu().numpy()
         assert np.array_equal(got, oracle_mod.sequential_ccl(img)), (w, h, n)
