@@ -83,28 +83,60 @@ __device__ __forceinline__ uint32_t gload(const uint32_t* p) {
 // semantics, restated over seam-touching roots only).  ~10 MB touched at 8192^2:
 // the walks hit L2 instead of scattered HBM sectors of the label buffer.
 struct Forest {
-    uint32_t* f;  // f[2n] = parent, f[2n+1] = key
-    __device__ __forceinline__ uint32_t parent(uint32_t n) const { return gload(f + 2 * size_t(n)); }
-    __device__ __forceinline__ uint32_t key(uint32_t n) const { return gload(f + 2 * size_t(n) + 1); }
-    __device__ __forceinline__ uint32_t find(uint32_t x) const {
-        uint32_t p = parent(x);
-        while (p != x) {
-            const uint32_t gp = parent(p);
-            if (gp == p) return p;
-            f[2 * size_t(x)] = gp;  // path halving (ancestor only)
-            x = gp;
-            p = parent(x);
+    uint32_t* f;  // f[2n] = parent, f[2n+1] = key (one 8-byte load gives both)
+    __device__ __forceinline__ uint2 node(uint32_t n) const {
+        uint2 v;
+        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(f + 2 * size_t(n))
+                     : "memory");
+        return v;
+    }
+    __device__ __forceinline__ uint32_t key(uint32_t n) const { return node(n).y; }
+    // Root of x and the root's {parent, key}.
+    __device__ __forceinline__ uint32_t find(uint32_t x, uint2& v) const {
+        v = node(x);
+        while (v.x != x) {
+            x = v.x;
+            v = node(x);
         }
         return x;
     }
+    __device__ __forceinline__ uint32_t find(uint32_t x) const {
+        uint2 v;
+        return find(x, v);
+    }
+    // find + path compression of x itself (later walks through x take one hop)
+    __device__ __forceinline__ uint2 find_compress(uint32_t x) const {
+        uint2 v;
+        const uint32_t r = find(x, v);
+        if (r != x) f[2 * size_t(x)] = r;
+        return v;
+    }
+    // Min-key union: the root with the larger key is linked below the other
+    // one with a CAS on its parent; both sides climb in lockstep so their
+    // loads overlap (the common case is one load per side, then the CAS).
     __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
+        uint2 A = node(a), B = node(b);
         for (;;) {
-            a = find(a);
-            b = find(b);
+            bool ca = A.x != a, cb = B.x != b;
+            while (ca || cb) {
+                uint2 An = A, Bn = B;
+                if (ca) An = node(A.x);
+                if (cb) Bn = node(B.x);
+                // (no path halving here: at high density every union climbs
+                // through the same few hot nodes and the extra stores thrash)
+                if (ca) { a = A.x; A = An; ca = A.x != a; }
+                if (cb) { b = B.x; B = Bn; cb = B.x != b; }
+            }
             if (a == b) return;
-            const uint32_t ka = key(a), kb = key(b);
-            if (ka < kb) { const uint32_t t = a; a = b; b = t; }  // a: the larger key
-            if (atomicCAS(f + 2 * size_t(a), a, b) == a) return;
+            if (A.y < B.y) {  // a: the root with the larger key
+                const uint32_t t = a; a = b; b = t;
+                const uint2 T = A; A = B; B = T;
+            }
+            const uint32_t old = atomicCAS(f + 2 * size_t(a), a, b);
+            if (old == a) return;
+            a = old;  // a was linked meanwhile: continue from its new parent
+            A = node(a);
+            B = node(b);
         }
     }
 };

@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
     const Forest fst = forest_of<C>(work, ntiles);
-    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.key(fst.find(t * uint32_t(C::MAXF) + k));
+    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.find_compress(t * uint32_t(C::MAXF) + k).y;
 }
 
 // ------------------------------------------------------------------ kernel (e)
