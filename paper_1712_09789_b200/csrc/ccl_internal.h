@@ -19,6 +19,12 @@
 #ifndef CCL_ULCAP
 #define CCL_ULCAP 128  // union-list entries per warp in kernel (a)
 #endif
+#ifndef CCL_HINTS
+#define CCL_HINTS 1  // L2 evict-first / evict-last policies on streams vs hand-off data
+#endif
+#ifndef CCL_DISCARD
+#define CCL_DISCARD 0  // kernel (e) discards consumed hand-off lines from L2
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

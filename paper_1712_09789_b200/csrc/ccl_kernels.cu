@@ -54,7 +54,8 @@ struct Cfg {
     static constexpr int W_LIST = W_PF + MW / 2;
     static constexpr int W_REC = W_LIST + MAXF;
     static constexpr int W_TBL = W_REC + 2 * TW + 2 * TH;
-    static constexpr int TILE_WORDS = W_TBL + PX / 2;  // table sized for pixel nodes (worst case)
+    static constexpr int TILE_WORDS = (W_TBL + PX / 2 + 31) / 32 * 32;  // table sized for pixel nodes; 128B lines
+    static_assert((2 * MAXF) % 32 == 0, "per-tile forest segments are whole 128B lines");
     static constexpr int S1_BYTES = (W_LIST - W_HEAD) * 4;  // head + masks + prefixes: one bulk copy
     // After the tiles: the COMPACT global forest, one {parent, key} u32 pair per
     // possible seam-touching root (node n = tile * MAXF + rank, key = the root's
@@ -213,6 +214,11 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(sdst)),
@@ -316,7 +322,10 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
 
     auto issue_at = [&](const TileId& q) {  // TMA 2-D tile load, OOB -> 0 == background
         mbar_expect_tx(bar, C::PX);
-        tma_load_3d(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar);
+        if (CCL_HINTS)
+            tma_load_3d_hint(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar, policy_evict_first());
+        else
+            tma_load_3d(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar);
     };
     if (TMA && tid == 0) {
         prefetch_tmap(&tm_img);
@@ -577,8 +586,9 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         __syncthreads();
         CCL_PH(7);
         if (tid == 0) {
-            bulk_store(wt + C::W_MASK, M, C::MW * 6);  // masks + u16 prefixes (contiguous)
-            if (nodes) bulk_store(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u);
+            const uint64_t keep = CCL_HINTS ? policy_evict_last() : policy_evict_normal();  // hand-off to (e)
+            bulk_store_hint(wt + C::W_MASK, M, C::MW * 6, keep);  // masks + u16 prefixes (contiguous)
+            if (nodes) bulk_store_hint(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u, keep);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
 
@@ -787,11 +797,23 @@ __global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUte
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg);  // OOB clipped
+                if (CCL_HINTS)
+                    tma_store_3d_hint(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg,
+                                      policy_evict_first());  // OOB clipped; labels stream out
+                else
+                    tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
         __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
+        if (CCL_DISCARD) {  // this tile's hand-off data (work tile + its forest segment) is dead:
+            // drop the dirty lines from L2 instead of writing them back
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(work_tile<C>(const_cast<uint32_t*>(work), t));
+            for (int i = tid; i < C::TILE_WORDS / 32; i += C::NT) discard_l2(base + 128 * i);
+            const uint8_t* fb = reinterpret_cast<const uint8_t*>(work + size_t(ntiles) * C::TILE_WORDS +
+                                                                 size_t(t) * 2 * C::MAXF);
+            for (int i = tid; i < 2 * C::MAXF / 32; i += C::NT) discard_l2(fb + 128 * i);
+        }
     }
     if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
