@@ -70,6 +70,7 @@ struct ccl_ctx {
     void* d_work = nullptr;     // kernel (a) -> (e) hand-off buffer
     size_t d_work_bytes = 0;
     ccl_timing last{};
+    bool last_split = false;
 };
 
 namespace {
@@ -136,12 +137,15 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
     return CCL_OK;
 }
 
-ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events) {
+// `split`: also time each kernel group (events between the launches break the
+// programmatic-dependent-launch chaining, so only timed calls pay for them).
+ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events, bool split = false) {
+    ctx->last_split = events && split;
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[0], a.stream));
     CCL_CHECK(cclk::launch_local(a));
-    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[1], a.stream));
+    if (ctx->last_split) CCL_CHECK(cudaEventRecord(ctx->ev[1], a.stream));
     CCL_CHECK(cclk::launch_seams(a));
-    if (events) CCL_CHECK(cudaEventRecord(ctx->ev[2], a.stream));
+    if (ctx->last_split) CCL_CHECK(cudaEventRecord(ctx->ev[2], a.stream));
     CCL_CHECK(cclk::launch_final(a));
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[3], a.stream));
     return CCL_OK;
@@ -150,9 +154,11 @@ ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events) {
 ccl_status read_timing(ccl_ctx* ctx, ccl_timing* t) {
     CCL_CHECK(cudaEventSynchronize(ctx->ev[3]));
     ccl_timing r{};
-    CCL_CHECK(cudaEventElapsedTime(&r.local_ms, ctx->ev[0], ctx->ev[1]));
-    CCL_CHECK(cudaEventElapsedTime(&r.merge_ms, ctx->ev[1], ctx->ev[2]));
-    CCL_CHECK(cudaEventElapsedTime(&r.final_ms, ctx->ev[2], ctx->ev[3]));
+    if (ctx->last_split) {
+        CCL_CHECK(cudaEventElapsedTime(&r.local_ms, ctx->ev[0], ctx->ev[1]));
+        CCL_CHECK(cudaEventElapsedTime(&r.merge_ms, ctx->ev[1], ctx->ev[2]));
+        CCL_CHECK(cudaEventElapsedTime(&r.final_ms, ctx->ev[2], ctx->ev[3]));
+    }
     CCL_CHECK(cudaEventElapsedTime(&r.total_ms, ctx->ev[0], ctx->ev[3]));
     ctx->last = r;
     if (t) *t = r;
@@ -236,7 +242,7 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
     if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
     if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, 1))) return s;
     a.work = static_cast<uint32_t*>(ctx->d_work);
-    if (ccl_status s = run_pipeline(ctx, a, true)) return s;
+    if (ccl_status s = run_pipeline(ctx, a, true, sync != 0)) return s;
     if (sync) return read_timing(ctx, timing);
     return CCL_OK;
 }

@@ -25,6 +25,9 @@
 #ifndef CCL_DISCARD
 #define CCL_DISCARD 0  // kernel (e) discards consumed hand-off lines from L2
 #endif
+#ifndef CCL_PDL
+#define CCL_PDL 1  // programmatic dependent launch of kernels (d), (d2), (e)
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

@@ -209,6 +209,11 @@ struct TileWalk {
     }
 };
 
+// Programmatic dependent launch: a dependent grid may be launched while its
+// predecessor drains; it must wait for the predecessor before touching its output.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
                  "r"(bytes)
@@ -621,6 +626,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     CCL_PH_DONE();
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------ kernel (d)
@@ -634,6 +640,8 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
     const uint32_t fz = blockIdx.y;
     const Forest fst = forest_of<C>(work, ntiles);
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint32_t nh = (g.nty - 1) * g.ntx * HC;
     const uint32_t nv = (g.ntx - 1) * g.nty * VC;
@@ -672,6 +680,8 @@ template <class C>
 __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t ntiles) {
     const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    pdl_wait();
+    pdl_trigger();
     if (t >= ntiles) return;
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
@@ -709,8 +719,9 @@ __global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUte
         if (lb) bulk_load(s2buf(j), wt + C::W_LIST, lb, &b2[j]);
         if (tb) bulk_load(s2buf(j) + C::MAXF, wt + C::W_TBL, tb, &b2[j]);
     };
+    if (tid == 0 && TMA_ST) prefetch_tmap(&tm_lab);
+    pdl_wait();
     if (tid == 0) {
-        if (TMA_ST) prefetch_tmap(&tm_lab);
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
         for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
         const uint32_t t0 = blockIdx.x;
@@ -852,6 +863,23 @@ static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntil
 
 static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
 
+// Launch with programmatic stream serialization (the kernel calls pdl_wait()
+// before reading what the previous kernel in the stream produced).
+template <class K, class... Args>
+static cudaError_t launch_pdl(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = CCL_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int VAR>
 static cudaError_t launch_local_v(const LaunchArgs& a) {
     using C = TileCfg;
@@ -885,19 +913,21 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
     using C = TileCfg;
     using E = ELayout<C, RUNS>;
     const uint32_t nt = tile_count(a);
-    k_resolve<C><<<unsigned((uint64_t(nt) * 32 + 255) / 256), 256, 0, a.stream>>>(a.work, a.g, nt);
+    cudaError_t e = launch_pdl(k_resolve<C>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
+                               a.g, nt);
+    if (e != cudaSuccess) return e;
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
-        k<<<persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1), C::NT, E::SMEM, a.stream>>>(a.tm_lab, a.labels,
-                                                                                             a.work, a.g, nt);
+        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
+                       a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
         auto k = k_final<C, RUNS, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
-        k<<<persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 2 : 3), C::NT, E::SMEM, a.stream>>>(a.tm_lab, a.labels,
-                                                                                             a.work, a.g, nt);
+        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 2 : 3)), C::NT, E::SMEM, a.stream,
+                       a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_final(const LaunchArgs& a) {
@@ -909,7 +939,8 @@ cudaError_t launch_seams(const LaunchArgs& a) {
     const uint64_t warps = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
     if (warps == 0) return cudaSuccess;
     const dim3 grid(unsigned((warps * 32 + 255) / 256), a.nframes);
-    k_seams<C><<<grid, 256, 0, a.stream>>>(a.work, a.g, tile_count(a));
+    const cudaError_t e = launch_pdl(k_seams<C>, grid, 256, 0, a.stream, a.work, a.g, tile_count(a));
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
