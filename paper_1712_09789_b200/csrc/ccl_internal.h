@@ -8,7 +8,7 @@
 
 // GPU tile = CCL_TILE_WX x CCL_TILE_WY warps, each warp a 32x32 pixel sub-tile.
 #ifndef CCL_JUMP
-#define CCL_JUMP 2  // pointer-jumping rounds over the coarse forest in kernel (a)
+#define CCL_JUMP 1  // pointer-jumping rounds over the coarse forest in kernel (a)
 #endif
 #ifndef CCL_WAVE
 #define CCL_WAVE 0  // barrier between flatten waves in kernel (a)
