@@ -28,6 +28,15 @@
 #ifndef CCL_PDL
 #define CCL_PDL 1  // programmatic dependent launch of kernels (d), (d2), (e)
 #endif
+#ifndef CCL_SEAM_MATCH
+#define CCL_SEAM_MATCH 1  // kernel (d): one union per distinct local-root pair per warp
+#endif
+#ifndef CCL_COARSE2
+#define CCL_COARSE2 1  // kernel (a) coarse scan as two loops (root codes, then links)
+#endif
+#ifndef CCL_JUMPBAR
+#define CCL_JUMPBAR 0
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

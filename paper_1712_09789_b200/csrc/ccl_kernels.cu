@@ -417,6 +417,26 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         uint32_t first = 0u;                                   // overlaps handled by a coarse link
         if (VAR == 0) first = os & ~lower_in_run(m, o) & ~((st & 1u) ? 0u : (m & ~(m + 1u)));
         if (VAR == 2) first = o;
+#if CCL_COARSE2
+        {
+            // every node starts as a root carrying its position ...
+            uint16_t* dst = P + pfx;
+            uint32_t tt = st;
+            while (tt) {
+                const uint32_t b = __ffs(tt) - 1;
+                tt &= tt - 1;
+                *dst++ = node_t(kRoot | (rowpos + b));
+            }
+            // ... then the coarse links overwrite the linked ones: one per
+            // first-overlap bit f (C2FL) / fg pixel with fg above (CC2FL)
+            uint32_t ff = first;
+            while (ff) {
+                const uint32_t f = __ffs(ff) - 1;
+                ff &= ff - 1;
+                P[node_of(pfx, st, f)] = node_t(node_of(upfx, ust, f));
+            }
+        }
+#else
         {
             uint32_t tt = st, id = pfx;
             while (tt) {
@@ -435,6 +455,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 ++id;
             }
         }
+#endif
         // refinement pairs (run, upper run) not covered by a coarse link go to
         // this warp's union list, so the unions are spread over all 32 lanes
         // instead of serialising on the lanes that own many of them
@@ -485,7 +506,9 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                         if (id < nodes && !(pp[k] & kRoot)) vP[id] = node_t(pp[k]);
                     }
                 }
-                __syncthreads();
+                // no barrier after the last round: jumps and unions only ever
+                // replace an entry by an ancestor, and unions CAS root entries only
+                if (j + 1 < CCL_JUMP || CCL_JUMPBAR) __syncthreads();
                 CCL_PH(3);
             }
         }
@@ -669,7 +692,15 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
     const bool fg = (a != kBG) && (b != kBG);
     bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
     if (lane == 0) prev = c > 0 && ra[i - 1] != kBG && rb[i - 1] != kBG;
-    if (fg && !prev) fst.unite(a, b);
+    bool act = fg && !prev;
+#if CCL_SEAM_MATCH
+    // one union per distinct (a, b) pair of local roots in the warp: the same
+    // two components often meet several times along 32 seam pixels
+    const uint64_t key = act ? (uint64_t(a) << 32 | b) : ~0ull;
+    const uint32_t same = __match_any_sync(0xffffffffu, key);
+    act = act && (__ffs(same) - 1 == lane);
+#endif
+    if (act) fst.unite(a, b);
 }
 
 // ------------------------------------------------------------------ kernel (d2)
