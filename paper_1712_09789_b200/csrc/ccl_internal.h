@@ -37,6 +37,15 @@
 #ifndef CCL_JUMPBAR
 #define CCL_JUMPBAR 0
 #endif
+#ifndef CCL_CARVEOUT
+#define CCL_CARVEOUT 100  // preferred shared-memory carveout (%) of kernels (a) and (e)
+#endif
+#ifndef CCL_EMINB
+#define CCL_EMINB 2
+#endif
+#ifndef CCL_ORDERED
+#define CCL_ORDERED 0  // kernel (a) node passes: contiguous id range per warp, in order
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

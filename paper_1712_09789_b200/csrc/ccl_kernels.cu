@@ -490,6 +490,24 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
 #pragma unroll 1
             for (int j = 0; j < CCL_JUMP; ++j) {
                 volatile node_t* vP = P;
+#if CCL_ORDERED
+                // each warp sweeps a contiguous id range in order (32 ids per
+                // step): a node's parent, one or two rows up, was usually jumped
+                // by this warp a step earlier, so the jumps compound
+                {
+                    const uint32_t chunk = ((nodes + C::NWARP - 1) / C::NWARP + 31) & ~31u;
+                    const uint32_t lo = warp * chunk, hi = min(lo + chunk, nodes);
+                    for (uint32_t base = lo; base < hi; base += 32) {
+                        const uint32_t id = base + lane;
+                        if (id < hi) {
+                            const uint32_t p = vP[id];
+                            const uint32_t pp = (p & kRoot) ? p : vP[p];
+                            if (!(pp & kRoot)) vP[id] = node_t(pp);
+                        }
+                        __syncwarp();
+                    }
+                }
+#else
                 // CCL_ILP independent nodes per thread in flight (latency-bound pass)
                 for (uint32_t base = tid; base < nodes; base += CCL_ILP * C::NT) {
                     uint32_t p[CCL_ILP], pp[CCL_ILP];
@@ -506,6 +524,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                         if (id < nodes && !(pp[k] & kRoot)) vP[id] = node_t(pp[k]);
                     }
                 }
+#endif
                 // no barrier after the last round: jumps and unions only ever
                 // replace an entry by an ancestor, and unions CAS root entries only
                 if (j + 1 < CCL_JUMP || CCL_JUMPBAR) __syncthreads();
@@ -595,6 +614,26 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         // already rewritten (parents always have smaller ids) end walks early.
         {
             volatile node_t* vP = P;
+#if CCL_ORDERED
+            // contiguous id range per warp, in order: parents one or two rows up
+            // were rewritten by this warp a step or two earlier, so most walks
+            // take one hop
+            const uint32_t chunk = ((nodes + C::NWARP - 1) / C::NWARP + 31) & ~31u;
+            const uint32_t lo = warp * chunk, hi = min(lo + chunk, nodes);
+            for (uint32_t base = lo; base < hi; base += 32) {
+                const uint32_t id = base + lane;
+                if (id < hi) {
+                    uint32_t p = vP[id];
+                    if (!(p & kRoot)) {
+                        do {
+                            p = vP[p];
+                        } while (!(p & kRoot));
+                        vP[id] = node_t(p);
+                    }
+                }
+                __syncwarp();
+            }
+#else
             for (uint32_t id = tid; id < nodes; id += C::NT) {
                 uint32_t p = vP[id];
                 if (!(p & kRoot)) {
@@ -604,6 +643,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                     vP[id] = node_t(p);
                 }
             }
+#endif
         }
         const uint32_t nf = FR[0];
         if (tid == 0) {
@@ -727,7 +767,7 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
 // swizzled staging tile and writes it with one TMA store: every label is
 // written exactly once and the image is never re-read.
 template <class C, bool RUNS, bool TMA_ST>
-__global__ void __launch_bounds__(C::NT, 2) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+__global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
                                                     const uint32_t* work, Geo g, uint32_t ntiles) {
     using E = ELayout<C, RUNS>;
     uint8_t* smem = aligned_smem();
@@ -919,6 +959,7 @@ static cudaError_t launch_local_v(const LaunchArgs& a) {
     if (a.tma_load) {
         auto k = k_local<C, VAR, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
         k<<<persistent_grid(k, C::NT, A::SMEM, nt, VAR), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
                                                                                        a.work, a.g, nt);
     } else {
@@ -950,6 +991,7 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
         e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
