@@ -123,6 +123,21 @@ ccl_status ccl_compact_device(ccl_ctx* ctx, const uint32_t* d_raw, uint32_t w, u
                               uint32_t* d_scratch, uint64_t* k_out, void* stream);
 size_t ccl_compact_scratch_words(uint32_t w, uint32_t h);
 
+/* ---- Label-map files (reference proj/src/label_io.cpp:27-94) ----
+ * ccl_label_to_cclm: label `img` (host, w*h bytes) on the device, compact on
+ * the device and write a CCLM file ("CCLM", version 1, W, H as u32 LE, then
+ * W*H compacted u32 LE labels); device->host copies overlap the file writes.
+ * *k_out (may be NULL) = number of components.  Blocking. */
+ccl_status ccl_label_to_cclm(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, int variant, const char* path,
+                             uint64_t* k_out);
+/* Host-only (no device needed): the reference's write_label_map (compacts
+ * first; format 0 raw CCLM, 1 csv, 2 pgm16) and read_label_map (CCLM).  On
+ * error they return CCL_EINVAL and ccl_io_last_error() says why. */
+ccl_status ccl_write_label_map(const uint32_t* labels, uint32_t w, uint32_t h, int compacted, int format,
+                               const char* path);
+ccl_status ccl_read_label_map(const char* path, uint32_t* labels, size_t capacity, uint32_t* w, uint32_t* h);
+const char* ccl_io_last_error(void);
+
 /* Tile geometry used by the kernels (for docs / tests). */
 void ccl_tile_shape(uint32_t* tile_w, uint32_t* tile_h);
 /* Number of kernel launches one ccl_label_device call makes. */

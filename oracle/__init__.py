@@ -93,6 +93,9 @@ def _load_ref():
         lib.ref_label_image.restype = ctypes.c_int
         lib.ref_sequential_ccl.argtypes = [_u8p, ctypes.c_uint32, ctypes.c_uint32, _u32p]
         lib.ref_sequential_ccl.restype = ctypes.c_int
+        lib.ref_write_label_map.argtypes = [_u32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_char_p]
+        lib.ref_write_label_map.restype = ctypes.c_int
         lib.ref_hardware_concurrency.argtypes = []
         lib.ref_hardware_concurrency.restype = ctypes.c_uint
         _ref = lib
@@ -190,6 +193,18 @@ def ref_sequential_ccl(img: np.ndarray) -> np.ndarray:
     if _load_ref().ref_sequential_ccl(_p8(img), w, h, _p32(out)) != 0:
         raise RuntimeError("reference sequential_ccl failed")
     return out
+
+
+def ref_write_label_map(labels: np.ndarray, path: str, fmt: str = "raw", compacted: bool = False) -> None:
+    """The reference's write_label_map (label_io.cpp:66-76) on a raw or compacted map.
+    Only "raw" is safe to call in-process (csv/pgm16 format through iostreams,
+    which crash with the libstdc++ state of a Python process)."""
+    lab = np.ascontiguousarray(labels, dtype=np.uint32)
+    h, w = lab.shape
+    rc = _load_ref().ref_write_label_map(_p32(lab), w, h, int(compacted), {"raw": 0, "csv": 1, "pgm16": 2}[fmt],
+                                         path.encode())
+    if rc != 0:
+        raise ValueError("reference write_label_map failed")
 
 
 def ref_hardware_concurrency() -> int:

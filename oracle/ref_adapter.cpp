@@ -12,6 +12,7 @@
 #include <thread>
 
 #include "ccl/generate.hpp"
+#include "ccl/label_io.hpp"
 #include "ccl/oracle.hpp"
 #include "ccl/pipeline.hpp"
 
@@ -84,5 +85,21 @@ int ref_sequential_ccl(const std::uint8_t* img, std::uint32_t w, std::uint32_t h
 }
 
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// write_label_map (label_io.cpp:66-76): format 0 raw, 1 csv, 2 pgm16
+int ref_write_label_map(const std::uint32_t* labels, std::uint32_t w, std::uint32_t h, int compacted, int format,
+                        const char* path) {
+    try {
+        ccl::LabelMap lm(w, h);
+        std::memcpy(lm.labels.data(), labels, lm.labels.size() * 4);
+        lm.compacted = compacted != 0;
+        ccl::write_label_map(lm, path, format == 1 ? ccl::LabelMapFormat::csv
+                                                   : format == 2 ? ccl::LabelMapFormat::pgm16
+                                                                 : ccl::LabelMapFormat::raw);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
 
 }  // extern "C"

@@ -30,7 +30,7 @@ import numpy as np
 __all__ = [
     "BG", "BlockConfig", "Variant", "LabelMap", "RunReport", "DeviceError", "label_image", "compact_labels",
     "random_image", "pattern_image", "label_device", "label_batch_device", "compact_device", "Context",
-    "tile_shape", "lib_path",
+    "tile_shape", "lib_path", "write_label_map", "read_label_map", "label_to_cclm",
 ]
 
 BG = 0xFFFFFFFF
@@ -79,6 +79,10 @@ _sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _
 _sig("ccl_strip_seam_resolve", _c, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
 _sig("ccl_strip_final", _c, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
 _sig("ccl_strip_scratch_words", _sz, _u32, _u32)
+_sig("ccl_label_to_cclm", _c, _vp, _u8p, _u32, _u32, _c, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64))
+_sig("ccl_write_label_map", _c, _u32p, _u32, _u32, _c, _c, ctypes.c_char_p)
+_sig("ccl_read_label_map", _c, ctypes.c_char_p, _u32p, _sz, _u32p, _u32p)
+_sig("ccl_io_last_error", ctypes.c_char_p)
 _sig("ccl_work_bytes", _sz, _u32, _u32, _u32)
 _sig("ccl_compact_device", _c, _vp, _vp, _u32, _u32, _vp, _vp, ctypes.POINTER(ctypes.c_uint64), _vp)
 _sig("ccl_compact_scratch_words", _sz, _u32, _u32)
@@ -91,6 +95,7 @@ _sig("ccl_version", ctypes.c_char_p)
 
 C_ABI_SYMBOLS = [
     "ccl_ctx_create", "ccl_ctx_destroy", "ccl_ctx_stream", "ccl_label_device", "ccl_label_host", "ccl_label_batch",
+    "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
     "ccl_launches_per_label", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
@@ -275,6 +280,43 @@ def compact_labels(lm: LabelMap) -> LabelMap:
     out = np.zeros(raw.shape, dtype=np.uint32)
     out[fg] = np.searchsorted(roots, raw[fg]).astype(np.uint32) + 1
     return LabelMap(lm.width, lm.height, out.reshape(lm.labels.shape), True)
+
+
+# ---------------------------------------------------------------- label-map files
+_FORMATS = {"raw": 0, "csv": 1, "pgm16": 2}
+
+
+def write_label_map(lm: LabelMap, path: str, fmt: str = "raw") -> None:
+    """label_io.cpp:66-76: compact, then write raw CCLM / csv / pgm16 (host only).
+    ValueError for an unknown format or an I/O / overflow failure."""
+    if fmt not in _FORMATS:
+        raise ValueError(f"unknown label map format: {fmt}")
+    lab = np.ascontiguousarray(lm.labels, dtype=np.uint32)
+    rc = _lib.ccl_write_label_map(lab.ctypes.data_as(_u32p), lm.width, lm.height, int(lm.compacted),
+                                  _FORMATS[fmt], os.fsencode(path))
+    if rc != 0:
+        raise ValueError(_lib.ccl_io_last_error().decode())
+
+
+def read_label_map(path: str) -> LabelMap:
+    """label_io.cpp:78-94: a compacted map from a CCLM file."""
+    w, h = _u32(), _u32()
+    if _lib.ccl_read_label_map(os.fsencode(path), None, 0, ctypes.byref(w), ctypes.byref(h)) != 0:
+        raise ValueError(_lib.ccl_io_last_error().decode())
+    out = np.empty((h.value, w.value), dtype=np.uint32)
+    if _lib.ccl_read_label_map(os.fsencode(path), out.ctypes.data_as(_u32p), out.size, None, None) != 0:
+        raise ValueError(_lib.ccl_io_last_error().decode())
+    return LabelMap(w.value, h.value, out, True)
+
+
+def label_to_cclm(img, path: str, variant="c2fl", device: int = 0) -> int:
+    """Label on the GPU, compact on the GPU, stream the CCLM file (device->host
+    copies overlap the file writes).  Returns the number of components K."""
+    a = _as_image(img)
+    k = ctypes.c_uint64()
+    _check(_lib.ccl_label_to_cclm(_ctx(device).handle, a.ctypes.data_as(_u8p), a.shape[1], a.shape[0],
+                                  int(Variant.parse(variant)), os.fsencode(path), ctypes.byref(k)))
+    return int(k.value)
 
 
 # ---------------------------------------------------------------- generators

@@ -68,6 +68,10 @@ struct ccl_ctx {
     uint32_t* h_lab = nullptr;  // pinned
     size_t h_lab_bytes = 0;
     void* d_work = nullptr;     // kernel (a) -> (e) hand-off buffer
+    uint32_t* d_aux = nullptr;  // compacted labels + compaction scratch (CCLM path)
+    size_t d_aux_bytes = 0;
+    uint8_t* h_ring = nullptr;  // pinned double buffer for chunked device->file copies
+    cudaEvent_t ring_ev[2] = {nullptr, nullptr};
     size_t d_work_bytes = 0;
     ccl_timing last{};
     bool last_split = false;
@@ -225,6 +229,10 @@ void ccl_ctx_destroy(ccl_ctx* c) {
     if (c->h_img) cudaFreeHost(c->h_img);
     if (c->h_lab) cudaFreeHost(c->h_lab);
     if (c->d_work) cudaFree(c->d_work);
+    if (c->d_aux) cudaFree(c->d_aux);
+    if (c->h_ring) cudaFreeHost(c->h_ring);
+    for (auto& e : c->ring_ev)
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 
@@ -421,6 +429,89 @@ ccl_status ccl_gen_pattern(uint8_t* out, int kind, uint32_t w, uint32_t h, uint3
     } catch (const std::exception& e) {
         return fail(CCL_ENOMEM, e.what());
     }
+}
+
+// ---------------------------------------------------------------- CCLM stream
+// Label on the device, compact on the device (pipeline.cpp:54-70), then copy
+// the compacted labels to a CCLM file (label_io.cpp:27-33 format) in chunks
+// through a pinned double buffer: the copy of chunk i+1 overlaps the write of
+// chunk i.
+ccl_status ccl_label_to_cclm(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, int variant, const char* path,
+                             uint64_t* k_out) {
+    if (!ctx || !img || !path) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
+    DeviceGuard dg(ctx->device);
+    const size_t px = size_t(w) * h;
+    const size_t pitch = (size_t(w) + 15) / 16 * 16;
+    if (ctx->d_img_bytes < pitch * h) {
+        if (ctx->d_img) cudaFree(ctx->d_img);
+        ctx->d_img = nullptr;
+        ctx->d_img_bytes = 0;
+        CCL_CHECK(cudaMalloc(&ctx->d_img, pitch * h));
+        ctx->d_img_bytes = pitch * h;
+    }
+    if (ctx->d_lab_bytes < px * 4) {
+        if (ctx->d_lab) cudaFree(ctx->d_lab);
+        ctx->d_lab = nullptr;
+        ctx->d_lab_bytes = 0;
+        CCL_CHECK(cudaMalloc(&ctx->d_lab, px * 4));
+        ctx->d_lab_bytes = px * 4;
+    }
+    const size_t aux = (px + cclk::compact_scratch_words(px)) * 4;
+    if (ctx->d_aux_bytes < aux) {
+        if (ctx->d_aux) cudaFree(ctx->d_aux);
+        ctx->d_aux = nullptr;
+        ctx->d_aux_bytes = 0;
+        CCL_CHECK(cudaMalloc(&ctx->d_aux, aux));
+        ctx->d_aux_bytes = aux;
+    }
+    constexpr size_t CH = size_t(16) << 20;  // bytes per chunk
+    if (!ctx->h_ring) {
+        CCL_CHECK(cudaMallocHost(&ctx->h_ring, 2 * CH));
+        for (auto& e : ctx->ring_ev) CCL_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CCL_CHECK(cudaMemcpy2DAsync(ctx->d_img, pitch, img, w, w, h, cudaMemcpyHostToDevice, ctx->stream));
+    if (ccl_status s = ccl_label_device(ctx, ctx->d_img, pitch, w, h, ctx->d_lab, variant, ctx->stream, 0, nullptr))
+        return s;
+    uint32_t* d_out = ctx->d_aux;
+    uint32_t* d_scr = ctx->d_aux + px;
+    CCL_CHECK(cclk::launch_compact(ctx->d_lab, px, d_out, d_scr, ctx->stream));
+    const size_t words = (px + 31) / 32, nb = (words + 1023) / 1024;
+    uint32_t k = 0;
+    CCL_CHECK(cudaMemcpyAsync(&k, d_scr + 2 * words + nb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(CCL_EINVAL, std::string("cannot open ") + path + " for writing");
+    unsigned char hdr[13] = {'C', 'C', 'L', 'M', 1};
+    for (int i = 0; i < 4; ++i) {
+        hdr[5 + i] = uint8_t(w >> (8 * i));
+        hdr[9 + i] = uint8_t(h >> (8 * i));
+    }
+    bool ok = std::fwrite(hdr, 1, 13, f) == 13;
+    const size_t total = px * 4, nchunks = (total + CH - 1) / CH;
+    auto issue = [&](size_t i) {
+        const size_t off = i * CH, n = std::min(CH, total - off);
+        cudaError_t e = cudaMemcpyAsync(ctx->h_ring + (i & 1) * CH, reinterpret_cast<uint8_t*>(d_out) + off, n,
+                                        cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[i & 1], ctx->stream);
+        return e;
+    };
+    cudaError_t e = issue(0);
+    for (size_t i = 0; ok && e == cudaSuccess && i < nchunks; ++i) {
+        if (i + 1 < nchunks) e = issue(i + 1);  // next copy in flight while this chunk is written
+        if (e != cudaSuccess) break;
+        e = cudaEventSynchronize(ctx->ring_ev[i & 1]);
+        if (e != cudaSuccess) break;
+        const size_t n = std::min(CH, total - i * CH);
+        ok = std::fwrite(ctx->h_ring + (i & 1) * CH, 1, n, f) == n;
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (e != cudaSuccess) return cuda_fail(e, "ccl_label_to_cclm");
+    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (!ok) return fail(CCL_EINVAL, std::string("write failed: ") + path);
+    if (k_out) *k_out = k;
+    return CCL_OK;
 }
 
 void ccl_tile_shape(uint32_t* tw, uint32_t* th) {

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "ccl/generate.hpp"
+#include "ccl/label_io.hpp"
 #include "ccl/pipeline.hpp"
 #include "ccl_cuda.h"
 
@@ -73,6 +74,14 @@ RunReport label_image(const BinaryImage& img, const BlockConfig& cfg, Variant va
                          int(variant), &ms));
     rep.wall_time = std::chrono::duration<double, std::milli>(double(ms));
     return rep;
+}
+
+std::uint64_t label_to_cclm(const BinaryImage& img, const std::string& path, Variant variant) {
+    if (img.data.size() != BinaryImage::check_size(img.width, img.height))
+        throw std::invalid_argument("image data size does not match width*height");
+    std::uint64_t k = 0;
+    check(ccl_label_to_cclm(thread_ctx(), img.data.data(), img.width, img.height, int(variant), path.c_str(), &k));
+    return k;
 }
 
 LabelMap compact_labels(const LabelMap& lm) {

@@ -35,3 +35,9 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def ccl():
+    import paper_1712_09789_b200 as ccl
+    return ccl
