@@ -6,7 +6,7 @@ One step = one labeling pass (kernels a-e) over one 8192x8192 u8 image
 resident in HBM; `value` = pixels / device time (CUDA events on the launching
 stream, L2 flushed by a 1 GiB read between steps).  N>1 (torchrun, one rank
 per GPU): weak-scaling strip mode, rank k labels rows [8192k, 8192(k+1)) of
-an 8192 x 8192N image (global raster labels) with the NCCL seam exchange
+random_image(8192, 8192N, 0.5, 0), generated on each GPU (global raster labels), with the NCCL seam exchange
 inside the timed step; value = total pixels / max-over-ranks step time.
 
 `e2e` = same metric through the public host API (ccl_label_host via
@@ -212,9 +212,9 @@ def main():
 
     if ws == 1:
         img_np = ccl.random_image(W, H, DENSITY, SEED)
-    else:
-        img_np = ccl.random_image(W, H, DENSITY, SEED + rank)  # strip k of the 8192 x 8192N image
-    img = torch.from_numpy(img_np).to(dev)
+        img = torch.from_numpy(img_np).to(dev)
+    else:  # rows [8192k, 8192(k+1)) of random_image(8192, 8192N, 0.5, 0), generated on this GPU
+        img = ccl.random_image_device(W, H, DENSITY, SEED, row0=rank * H, device=lrank)
     out = torch.empty((H, W), dtype=torch.uint32, device=dev)
     ctx = ccl.Context(lrank)
 
@@ -295,7 +295,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "Gpixels/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (reference xoshiro256** generator, seed 0)",
-            "config": {"workload": "random8192" if ws == 1 else f"strips 8192x{8192 * ws} (8192 rows/GPU)",
+            "config": {"workload": "random8192" if ws == 1 else
+                       f"strips of random_image(8192, {8192 * ws}, 0.5, 0) (8192 rows/GPU)",
                        "width": W, "height": H * ws, "density": DENSITY, "seed": SEED, "variant": args.variant,
                        "tile": list(ccl.tile_shape()), "l2_flush": "1 GiB read between timed steps",
                        "parallelism": "single GPU" if ws == 1 else f"{ws} strips, NCCL seam all-gather"},

@@ -123,6 +123,14 @@ ccl_status ccl_compact_device(ccl_ctx* ctx, const uint32_t* d_raw, uint32_t w, u
                               uint32_t* d_scratch, uint64_t* k_out, void* stream);
 size_t ccl_compact_scratch_words(uint32_t w, uint32_t h);
 
+/* random_image generated on the device: rows
+ * [row0, row0+h) of random_image(w, *, density, seed) as w*h bytes at d_out
+ * (pitch w, 16-byte aligned), byte-identical with ccl_gen_random / the
+ * reference generate.cpp:9-18 (xoshiro256** jump-ahead per chunk; row0 > 0
+ * gives one strip of a taller image).  Returns once the image is written. */
+ccl_status ccl_gen_random_device(ccl_ctx* ctx, uint8_t* d_out, uint32_t w, uint32_t h, uint32_t row0, double density,
+                                 uint64_t seed, void* stream);
+
 /* ---- Label-map files (reference proj/src/label_io.cpp:27-94) ----
  * ccl_label_to_cclm: label `img` (host, w*h bytes) on the device, compact on
  * the device and write a CCLM file ("CCLM", version 1, W, H as u32 LE, then

@@ -30,7 +30,7 @@ import numpy as np
 __all__ = [
     "BG", "BlockConfig", "Variant", "LabelMap", "RunReport", "DeviceError", "label_image", "compact_labels",
     "random_image", "pattern_image", "label_device", "label_batch_device", "compact_device", "Context",
-    "tile_shape", "lib_path", "write_label_map", "read_label_map", "label_to_cclm",
+    "tile_shape", "lib_path", "write_label_map", "read_label_map", "label_to_cclm", "random_image_device",
 ]
 
 BG = 0xFFFFFFFF
@@ -79,6 +79,7 @@ _sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _
 _sig("ccl_strip_seam_resolve", _c, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
 _sig("ccl_strip_final", _c, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
 _sig("ccl_strip_scratch_words", _sz, _u32, _u32)
+_sig("ccl_gen_random_device", _c, _vp, _vp, _u32, _u32, _u32, ctypes.c_double, ctypes.c_uint64, _vp)
 _sig("ccl_label_to_cclm", _c, _vp, _u8p, _u32, _u32, _c, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64))
 _sig("ccl_write_label_map", _c, _u32p, _u32, _u32, _c, _c, ctypes.c_char_p)
 _sig("ccl_read_label_map", _c, ctypes.c_char_p, _u32p, _sz, _u32p, _u32p)
@@ -95,7 +96,7 @@ _sig("ccl_version", ctypes.c_char_p)
 
 C_ABI_SYMBOLS = [
     "ccl_ctx_create", "ccl_ctx_destroy", "ccl_ctx_stream", "ccl_label_device", "ccl_label_host", "ccl_label_batch",
-    "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
+    "ccl_gen_random_device", "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
     "ccl_launches_per_label", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
@@ -326,6 +327,19 @@ _PATTERNS = {"stripes": 0, "spiral": 1, "blobs": 2, "checkerboard": 3}
 def random_image(w: int, h: int, density: float, seed: int) -> np.ndarray:
     out = np.empty((h, w), dtype=np.uint8)
     _check(_lib.ccl_gen_random(out.ctypes.data_as(_u8p), w, h, density, seed))
+    return out
+
+
+def random_image_device(w: int, h: int, density: float, seed: int, out=None, stream=None, device: int = 0,
+                        row0: int = 0):
+    """random_image generated on the GPU (xoshiro256** jump-ahead), byte-identical
+    with random_image; rows [row0, row0+h) of a taller image when row0 > 0.
+    Returns an (h, w) uint8 torch tensor on the device."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((h, w), dtype=torch.uint8, device=f"cuda:{device}")
+    _check(_lib.ccl_gen_random_device(_ctx(device).handle, out.data_ptr(), w, h, int(row0), float(density), int(seed),
+                                      _stream_ptr(stream)))
     return out
 
 

@@ -412,6 +412,18 @@ ccl_status ccl_gen_random(uint8_t* out, uint32_t w, uint32_t h, double density, 
     }
 }
 
+ccl_status ccl_gen_random_device(ccl_ctx* ctx, uint8_t* d_out, uint32_t w, uint32_t h, uint32_t row0, double density,
+                                 uint64_t seed, void* stream) {
+    if (!ctx || !d_out) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (!(density >= 0.0 && density <= 1.0)) return fail(CCL_EINVAL, "density must be in [0, 1]");
+    if (reinterpret_cast<uintptr_t>(d_out) % 16) return fail(CCL_EINVAL, "d_out must be 16-byte aligned");
+    DeviceGuard dg(ctx->device);
+    CCL_CHECK(cclk::launch_gen_random(d_out, uint64_t(w) * h, uint64_t(row0) * w, density, seed,
+                                      static_cast<cudaStream_t>(stream)));
+    return CCL_OK;
+}
+
 ccl_status ccl_gen_pattern(uint8_t* out, int kind, uint32_t w, uint32_t h, uint32_t period, double density,
                            uint64_t seed) {
     if (!out) return fail(CCL_EINVAL, "null argument");

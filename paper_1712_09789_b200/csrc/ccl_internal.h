@@ -98,6 +98,8 @@ cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* seam_all, uint32_
                                  uint32_t* labels, uint32_t* work, uint32_t* scratch, cudaStream_t s);
 cudaError_t launch_compact(const uint32_t* raw, size_t n, uint32_t* out, uint32_t* scratch, cudaStream_t s);
 size_t compact_scratch_words(size_t n);
+cudaError_t launch_gen_random(uint8_t* out, uint64_t n, uint64_t first, double density, uint64_t seed,
+                              cudaStream_t s);
 
 size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
 uint32_t* strip_area_ptr(uint32_t* work, const Geo& g);  // strip mode: [edge nodes 2W | edge roots 2W]

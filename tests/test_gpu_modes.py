@@ -159,3 +159,18 @@ def test_known_answer_32768(ccl, oracle_mod, known_answers):
     k, fg = oracle_mod.count(lab)
     assert (k, fg) == (ka["K"], ka["fg"])
     assert f"{oracle_mod.fnv1a64(lab):016x}" == ka["fnv1a64_raw"]
+
+
+@pytest.mark.gpu
+def test_random_image_device_matches_host(ccl):
+    # xoshiro256** jump-ahead per chunk, byte-identical with
+    # the host generator (reference generate.cpp:9-18)
+    for (w, h, d, s) in [(1, 1, 0.5, 0), (17, 3, 0.3, 7), (1920, 1080, 0.5, 1023), (2048, 2048, 0.1, 0),
+                         (4096, 1000, 0.9, 12345), (8192, 8192, 0.5, 0)]:
+        got = ccl.random_image_device(w, h, d, s).cpu().numpy()
+        full = ccl.random_image(w, h, d, s)
+        assert np.array_equal(got, full), (w, h, d, s)
+        if h >= 3:  # one strip of the same image
+            r0 = h // 3
+            strip = ccl.random_image_device(w, h - r0, d, s, row0=r0).cpu().numpy()
+            assert np.array_equal(strip, full[r0:]), (w, h, d, s, r0)
