@@ -46,6 +46,9 @@
 #ifndef CCL_ORDERED
 #define CCL_ORDERED 0  // kernel (a) node passes: contiguous id range per warp, in order
 #endif
+#ifndef CCL_L2PERSIST
+#define CCL_L2PERSIST 0  // persisting-L2 window over the work buffer for (a) and (e)
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

@@ -933,22 +933,57 @@ static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntil
 }
 
 static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
+static size_t work_bytes_used(const LaunchArgs& a) {
+    return size_t(tile_count(a)) * (size_t(TileCfg::TILE_WORDS) + 2 * size_t(TileCfg::MAXF)) * 4;
+}
 
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()
-// before reading what the previous kernel in the stream produced).
+// before reading what the previous kernel in the stream produced) and, with
+// CCL_L2PERSIST, a persisting-L2 access-policy window over the work buffer
+// (the hand-off between the kernels).
 template <class K, class... Args>
-static cudaError_t launch_pdl(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, Args... args) {
+static cudaError_t launch_ex(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, bool pdl, void* win,
+                             size_t win_bytes, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = CCL_PDL;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n++].val.programmaticStreamSerializationAllowed = CCL_PDL;
+    }
+#if CCL_L2PERSIST
+    if (win && win_bytes) {
+        static int max_win = -1, max_persist = -1;
+        if (max_win < 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(max_persist));
+        }
+        const size_t nb = win_bytes < size_t(max_win) ? win_bytes : size_t(max_win);
+        attr[n].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[n].val.accessPolicyWindow.base_ptr = win;
+        attr[n].val.accessPolicyWindow.num_bytes = nb;
+        attr[n].val.accessPolicyWindow.hitRatio = nb ? float(double(max_persist) / double(nb) > 1.0 ? 1.0 : double(max_persist) / double(nb)) : 0.f;
+        attr[n].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[n++].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+#else
+    (void)win;
+    (void)win_bytes;
+#endif
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = n;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <class K, class... Args>
+static cudaError_t launch_pdl(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, Args... args) {
+    return launch_ex(kernel, grid, threads, smem, s, true, nullptr, 0, args...);
 }
 
 template <int VAR>
@@ -960,8 +995,10 @@ static cudaError_t launch_local_v(const LaunchArgs& a) {
         auto k = k_local<C, VAR, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        k<<<persistent_grid(k, C::NT, A::SMEM, nt, VAR), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
-                                                                                       a.work, a.g, nt);
+        const cudaError_t e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, VAR)), C::NT, A::SMEM,
+                                        a.stream, false, a.work, work_bytes_used(a), a.tm_img, a.img, a.labels,
+                                        a.work, a.g, nt);
+        if (e != cudaSuccess) return e;
     } else {
         auto k = k_local<C, VAR, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
@@ -992,8 +1029,9 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
         auto k = k_final<C, RUNS, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
-                       a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
+        e = launch_ex(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
+                      true, a.work, work_bytes_used(a), a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g,
+                      nt);
     } else {
         auto k = k_final<C, RUNS, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
