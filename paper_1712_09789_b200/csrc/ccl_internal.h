@@ -49,6 +49,9 @@
 #ifndef CCL_L2PERSIST
 #define CCL_L2PERSIST 0  // persisting-L2 window over the work buffer for (a) and (e)
 #endif
+#ifndef CCL_TABLE_WAVES
+#define CCL_TABLE_WAVES 1  // barrier-separated waves of kernel (a)'s table pass
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

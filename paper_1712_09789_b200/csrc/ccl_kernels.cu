@@ -634,13 +634,20 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 __syncwarp();
             }
 #else
-            for (uint32_t id = tid; id < nodes; id += C::NT) {
-                uint32_t p = vP[id];
-                if (!(p & kRoot)) {
-                    do {
-                        p = vP[p];
-                    } while (!(p & kRoot));
-                    vP[id] = node_t(p);
+            // CCL_TABLE_WAVES waves of ids with a barrier between them: walks in
+            // a later wave stop at the already rewritten nodes of earlier waves
+            for (int wv = 0; wv < CCL_TABLE_WAVES; ++wv) {
+                const uint32_t lo = uint32_t((uint64_t(nodes) * wv) / CCL_TABLE_WAVES);
+                const uint32_t hi = uint32_t((uint64_t(nodes) * (wv + 1)) / CCL_TABLE_WAVES);
+                if (wv) __syncthreads();
+                for (uint32_t id = lo + tid; id < hi; id += C::NT) {
+                    uint32_t p = vP[id];
+                    if (!(p & kRoot)) {
+                        do {
+                            p = vP[p];
+                        } while (!(p & kRoot));
+                        vP[id] = node_t(p);
+                    }
                 }
             }
 #endif
