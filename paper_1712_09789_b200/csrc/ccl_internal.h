@@ -56,10 +56,13 @@
 #define CCL_PHASES 0
 #endif
 #ifndef CCL_MINB
-#define CCL_MINB 6  // min resident CTAs of kernel (a) (register cap)
+#define CCL_MINB 10  // min resident CTAs of kernel (a) (register cap)
+#endif
+#ifndef CCL_WPL
+#define CCL_WPL 2  // 32-px row words per lane in kernels (a) and (e)
 #endif
 #ifndef CCL_TILE_WX
-#define CCL_TILE_WX 4
+#define CCL_TILE_WX 2
 #endif
 #ifndef CCL_TILE_WY
 #define CCL_TILE_WY 2

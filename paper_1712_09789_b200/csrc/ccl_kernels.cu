@@ -37,17 +37,19 @@
 
 namespace cclk {
 
-template <int WX_, int WY_>
+template <int WX_, int WY_, int WPL_ = 1>
 struct Cfg {
-    static constexpr int WX = WX_, WY = WY_;
-    static constexpr int TW = 32 * WX, TH = 32 * WY, NT = 32 * WX * WY, NWARP = WX * WY;
+    static constexpr int WX = WX_, WY = WY_;  // warps across / down the tile
+    static constexpr int WPL = WPL_;          // 32-px row words per lane
+    static constexpr int WPR = WX * WPL;      // row words per tile row
+    static constexpr int TW = 32 * WPR, TH = 32 * WY, NT = 32 * WX * WY, NWARP = WX * WY;
     static constexpr int PX = TW * TH;
     static constexpr int MAXF = 2 * TW + 2 * TH;  // bound on seam-touching roots (one per boundary run)
     // work buffer (global) per tile, in u32 words:
     //   head [nF, nodes, -, -] | row-word masks | per-word node prefix (u16) |
     //   seam-root list (global index; resolved label after k_resolve) |
     //   seam records (local root of every border pixel: top, bottom, left, right) | node table (u16)
-    static constexpr int MW = TH * WX;  // row words
+    static constexpr int MW = TH * WPR;  // row words
     static constexpr int W_HEAD = 0;
     static constexpr int W_MASK = 4;
     static constexpr int W_PF = W_MASK + MW;
@@ -65,7 +67,13 @@ struct Cfg {
     static_assert(MW % 8 == 0, "16-byte alignment of the work-buffer sections");
 };
 
-using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY>;
+// Kernel (a)'s CTA layout; kernels (d), (d2) and the work-buffer layout only
+// depend on the tile shape.  Kernel (e) has its own warp layout over the same
+// tile (one 32-px word per lane): same TW, TH, MW, MAXF, hence the same work tile.
+using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY, CCL_WPL>;
+using ECfg = Cfg<CCL_TILE_WX * CCL_WPL, CCL_TILE_WY, 1>;
+static_assert(ECfg::TW == TileCfg::TW && ECfg::TH == TileCfg::TH && ECfg::TILE_WORDS == TileCfg::TILE_WORDS,
+              "kernel (e) must see kernel (a)'s work tiles");
 
 // Kernel (a) shared memory, per node granularity (runs: <= PX/2 nodes).
 template <class C, bool RUNS>
@@ -94,7 +102,7 @@ struct ELayout {
     static constexpr int S1_OFF = 0;
     static constexpr int S2_OFF = S1_OFF + 3 * S1;
     static constexpr int STG_OFF = ((S2_OFF + 2 * S2) + 1023) / 1024 * 1024;
-    static constexpr int BAR_OFF = STG_OFF + C::NWARP * 4096;
+    static constexpr int BAR_OFF = STG_OFF + C::NWARP * C::WPL * 4096;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;
 };
 
@@ -321,7 +329,8 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane;
-    const int col0 = wx * 32;
+    const int col0 = wx * 32 * C::WPL;  // first pixel column of this lane's words
+    const int wc0 = wx * C::WPL;        // first word column
     const Forest fst = forest_of<C>(work, ntiles);
     uint32_t* SE = strip_area<C>(work, ntiles);  // strip mode: edge-row nodes [top W | bottom W]
 
@@ -366,16 +375,19 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 M16[c] = static_cast<uint16_t>(eq1_mask16(q));
             }
         } else {
-            uint32_t mm = 0u;
             const uint32_t gy = y0 + row;
-            if (gy < g.H) {
-                const uint8_t* src = img + size_t(ti.fz) * g.frame_pitch + size_t(gy) * g.img_pitch;
-                for (int b = 0; b < 32; ++b) {
-                    const uint32_t gx = x0 + col0 + b;
-                    if (gx < g.W && src[gx] == 1) mm |= 1u << b;
+#pragma unroll
+            for (int k = 0; k < C::WPL; ++k) {
+                uint32_t mm = 0u;
+                if (gy < g.H) {
+                    const uint8_t* src = img + size_t(ti.fz) * g.frame_pitch + size_t(gy) * g.img_pitch;
+                    for (int b = 0; b < 32; ++b) {
+                        const uint32_t gx = x0 + col0 + 32 * k + b;
+                        if (gx < g.W && src[gx] == 1) mm |= 1u << b;
+                    }
                 }
+                M[row * C::WPR + wx * C::WPL + k] = mm;
             }
-            M[row * C::WX + wx] = mm;
         }
         __syncthreads();
         CCL_PH(1);
@@ -385,43 +397,59 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             issue_at(nx.cur);
         }
 
-        const uint32_t m = M[row * C::WX + wx];
-        const uint32_t lm = wx > 0 ? M[row * C::WX + wx - 1] : 0u;
-        const uint32_t um = row > 0 ? M[(row - 1) * C::WX + wx] : 0u;
-        const uint32_t lum = (row > 0 && wx > 0) ? M[(row - 1) * C::WX + wx - 1] : 0u;
-        const uint32_t st = word_starts<RUNS>(m, lm);
-        const uint32_t ust = word_starts<RUNS>(um, lum);
+        // this lane's WPL row words (row, wc0 + k), their left / upper neighbours
+        uint32_t m[C::WPL], lm[C::WPL], um[C::WPL], lum[C::WPL], st[C::WPL], ust[C::WPL];
+#pragma unroll
+        for (int k = 0; k < C::WPL; ++k) {
+            const int wc = wc0 + k;
+            m[k] = M[row * C::WPR + wc];
+            um[k] = row > 0 ? M[(row - 1) * C::WPR + wc] : 0u;
+            lm[k] = k > 0 ? m[k - 1] : (wc > 0 ? M[row * C::WPR + wc - 1] : 0u);
+            lum[k] = k > 0 ? um[k - 1] : ((row > 0 && wc > 0) ? M[(row - 1) * C::WPR + wc - 1] : 0u);
+            st[k] = word_starts<RUNS>(m[k], lm[k]);
+            ust[k] = word_starts<RUNS>(um[k], lum[k]);
+        }
 
         // ---- coarse row scan: node ids in tile raster order
-        uint32_t nodes;
-        const uint32_t pfx = tile_prefix<C>(__popc(st), CNT, BT, row, wx, wy, lane, &nodes);
-        PF16[row * C::WX + wx] = uint16_t(pfx);
-        uint32_t upfx = __shfl_up_sync(0xffffffffu, pfx, 1);
-        if (lane == 0) {  // word above belongs to the warp band above: prefix from the counts
+        uint32_t nodes, cnt = 0, ucnt0 = 0;
+#pragma unroll
+        for (int k = 0; k < C::WPL; ++k) cnt += __popc(st[k]);
+        const uint32_t pfx0 = tile_prefix<C>(cnt, CNT, BT, row, wx, wy, lane, &nodes);
+        uint32_t upfx0 = __shfl_up_sync(0xffffffffu, pfx0, 1);
+        if (lane == 0) {  // words above belong to the warp band above: prefix from the counts
             uint32_t rest = 0, left = 0;
 #pragma unroll
             for (int w = 0; w < C::WX; ++w) {
                 rest += (row > 0 && w >= wx) ? CNT[(row - 1) * C::WX + w] : 0u;
                 left += (w < wx) ? CNT[row * C::WX + w] : 0u;
             }
-            upfx = pfx - left - rest;
+            upfx0 = pfx0 - left - rest;
         }
-        const uint32_t rowpos = uint32_t(row * C::TW + col0);
+        (void)ucnt0;
+        uint32_t pfx[C::WPL], upfx[C::WPL];
+#pragma unroll
+        for (int k = 0; k < C::WPL; ++k) {
+            pfx[k] = k > 0 ? pfx[k - 1] + __popc(st[k - 1]) : pfx0;
+            upfx[k] = k > 0 ? upfx[k - 1] + __popc(ust[k - 1]) : upfx0;
+            PF16[row * C::WPR + wc0 + k] = uint16_t(pfx[k]);
+        }
 
         // ---- init + coarse column scan (plain stores, no atomics): every node is
         // its own parent, except that C2FL links a run to the upper run holding
-        // its first overlap inside this word and CC2FL links a pixel to the pixel above.
-        const uint32_t o = m & um;
-        const uint32_t ocont = (o & 1u) & ((lm & lum) >> 31);  // overlap continuing from the left word
-        const uint32_t os = (o & ~(o << 1)) & ~ocont;          // one bit per (node, upper node) overlap
-        uint32_t first = 0u;                                   // overlaps handled by a coarse link
-        if (VAR == 0) first = os & ~lower_in_run(m, o) & ~((st & 1u) ? 0u : (m & ~(m + 1u)));
-        if (VAR == 2) first = o;
-#if CCL_COARSE2
-        {
+        // its first overlap inside its word and CC2FL links a pixel to the pixel above.
+        uint32_t o[C::WPL], os[C::WPL], first[C::WPL];
+#pragma unroll
+        for (int k = 0; k < C::WPL; ++k) {
+            o[k] = m[k] & um[k];
+            const uint32_t ocont = (o[k] & 1u) & ((lm[k] & lum[k]) >> 31);  // overlap continuing from the left
+            os[k] = (o[k] & ~(o[k] << 1)) & ~ocont;                       // one bit per (node, upper node) overlap
+            first[k] = 0u;                                                // overlaps handled by a coarse link
+            if (VAR == 0) first[k] = os[k] & ~lower_in_run(m[k], o[k]) & ~((st[k] & 1u) ? 0u : (m[k] & ~(m[k] + 1u)));
+            if (VAR == 2) first[k] = o[k];
+            const uint32_t rowpos = uint32_t(row * C::TW + col0 + 32 * k);
             // every node starts as a root carrying its position ...
-            uint16_t* dst = P + pfx;
-            uint32_t tt = st;
+            uint16_t* dst = P + pfx[k];
+            uint32_t tt = st[k];
             while (tt) {
                 const uint32_t b = __ffs(tt) - 1;
                 tt &= tt - 1;
@@ -429,55 +457,43 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             }
             // ... then the coarse links overwrite the linked ones: one per
             // first-overlap bit f (C2FL) / fg pixel with fg above (CC2FL)
-            uint32_t ff = first;
+            uint32_t ff = first[k];
             while (ff) {
                 const uint32_t f = __ffs(ff) - 1;
                 ff &= ff - 1;
-                P[node_of(pfx, st, f)] = node_t(node_of(upfx, ust, f));
+                P[node_of(pfx[k], st[k], f)] = node_t(node_of(upfx[k], ust[k], f));
             }
         }
-#else
-        {
-            uint32_t tt = st, id = pfx;
-            while (tt) {
-                const uint32_t b = __ffs(tt) - 1;
-                tt &= tt - 1;
-                uint32_t par = id;
-                if (VAR == 0) {
-                    const uint32_t fb = first & (0xFFFFFFFFu << b);  // first overlaps at/after this run
-                    const uint32_t f = __ffs(fb) - 1;
-                    const uint32_t nxt = tt ? __ffs(tt) - 1 : 32u;   // next run start in this word
-                    if (fb && f < nxt) par = node_of(upfx, ust, f);
-                } else if (VAR == 2) {
-                    if ((um >> b) & 1u) par = node_of(upfx, ust, b);
-                }
-                P[id] = node_t(par == id ? (kRoot | (rowpos + b)) : par);
-                ++id;
-            }
-        }
-#endif
         // refinement pairs (run, upper run) not covered by a coarse link go to
         // this warp's union list, so the unions are spread over all 32 lanes
         // instead of serialising on the lanes that own many of them
-        uint32_t U = RUNS ? (os & ~first) : 0u;
+        uint32_t U[C::WPL];
+        uint32_t cu = 0;
+#pragma unroll
+        for (int k = 0; k < C::WPL; ++k) {
+            U[k] = RUNS ? (os[k] & ~first[k]) : 0u;
+            cu += __popc(U[k]);
+        }
         uint32_t* UL = reinterpret_cast<uint32_t*>(smem + A::UL_OFF) + warp * A::UL_CAP;
         uint32_t nul;
         {
-            const uint32_t cu = __popc(U);
             uint32_t inc = cu;
 #pragma unroll
-            for (int k = 1; k < 32; k <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, k);
-                if (lane >= k) inc += y;
+            for (int j = 1; j < 32; j <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, j);
+                if (lane >= j) inc += y;
             }
             const bool fits = inc <= uint32_t(A::UL_CAP);
             nul = __reduce_max_sync(0xffffffffu, fits ? inc : 0u);  // entries actually listed
             if (fits) {  // all of this lane's pairs fit: list them
                 uint32_t* dst = UL + (inc - cu);
-                while (U) {
-                    const uint32_t b = __ffs(U) - 1;
-                    U &= U - 1;
-                    *dst++ = node_of(pfx, st, b) | (node_of(upfx, ust, b) << 16);
+#pragma unroll
+                for (int k = 0; k < C::WPL; ++k) {
+                    while (U[k]) {
+                        const uint32_t b = __ffs(U[k]) - 1;
+                        U[k] &= U[k] - 1;
+                        *dst++ = node_of(pfx[k], st[k], b) | (node_of(upfx[k], ust[k], b) << 16);
+                    }
                 }
             }
         }
@@ -538,21 +554,24 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 const uint32_t pr = UL[k];
                 nunion(P, pr & 0xFFFFu, pr >> 16);
             }
-            if (!RUNS) U = (VAR == 3) ? o : 0u;  // NC2FL: every vertical pixel pair
-            while (U) {                           // pairs that did not fit in the list
-                const uint32_t b = __ffs(U) - 1;
-                U &= U - 1;
-                nunion(P, node_of(pfx, st, b), node_of(upfx, ust, b));
-            }
-            if (!RUNS) {  // horizontal pixel pairs (incl. the word boundary), minus closed 2x2 squares
-                const uint32_t hm = m & ((m << 1) | ((lm >> 31) & 1u));
-                const uint32_t hu = um & ((um << 1) | ((lum >> 31) & 1u));
-                uint32_t hp = (VAR == 2) ? (hm & ~hu) : hm;
-                while (hp) {
-                    const uint32_t b = __ffs(hp) - 1;
-                    hp &= hp - 1;
-                    const uint32_t id = node_of(pfx, st, b);
-                    nunion(P, id, id - 1);  // the left neighbour is the previous fg pixel in raster order
+#pragma unroll
+            for (int k = 0; k < C::WPL; ++k) {
+                uint32_t Uk = RUNS ? U[k] : ((VAR == 3) ? o[k] : 0u);  // NC2FL: every vertical pixel pair
+                while (Uk) {                                          // pairs that did not fit in the list
+                    const uint32_t b = __ffs(Uk) - 1;
+                    Uk &= Uk - 1;
+                    nunion(P, node_of(pfx[k], st[k], b), node_of(upfx[k], ust[k], b));
+                }
+                if (!RUNS) {  // horizontal pixel pairs (incl. the word boundary), minus closed 2x2 squares
+                    const uint32_t hm = m[k] & ((m[k] << 1) | ((lm[k] >> 31) & 1u));
+                    const uint32_t hu = um[k] & ((um[k] << 1) | ((lum[k] >> 31) & 1u));
+                    uint32_t hp = (VAR == 2) ? (hm & ~hu) : hm;
+                    while (hp) {
+                        const uint32_t b = __ffs(hp) - 1;
+                        hp &= hp - 1;
+                        const uint32_t id = node_of(pfx[k], st[k], b);
+                        nunion(P, id, id - 1);  // the left neighbour is the previous fg pixel in raster order
+                    }
                 }
             }
         }
@@ -567,8 +586,8 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
         {
-            const uint32_t top_n = PF16[C::WX];               // nodes in row 0
-            const uint32_t bot0 = PF16[(C::TH - 1) * C::WX];  // first node of the last row
+            const uint32_t top_n = PF16[C::WPR];               // nodes in row 0
+            const uint32_t bot0 = PF16[(C::TH - 1) * C::WPR];  // first node of the last row
             const uint32_t n1 = has_top ? top_n : 0u;
             const uint32_t n2 = n1 + (has_bot ? nodes - bot0 : 0u);
             const uint32_t n3 = n2 + (has_left ? uint32_t(C::TH) : 0u);
@@ -581,14 +600,14 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                     id = bot0 + (i - n1);
                 } else if (i < n3) {
                     const uint32_t r = i - n2;
-                    if (!(M[r * C::WX] & 1u)) continue;
-                    id = PF16[r * C::WX];
+                    if (!(M[r * C::WPR] & 1u)) continue;
+                    id = PF16[r * C::WPR];
                 } else {
                     const uint32_t r = i - n3;
-                    const uint32_t wl = M[r * C::WX + C::WX - 1];
+                    const uint32_t wl = M[r * C::WPR + C::WPR - 1];
                     if (!(wl >> 31)) continue;
-                    const uint32_t wll = C::WX > 1 ? M[r * C::WX + C::WX - 2] : 0u;
-                    id = node_of(PF16[r * C::WX + C::WX - 1], word_starts<RUNS>(wl, wll), 31);
+                    const uint32_t wll = C::WPR > 1 ? M[r * C::WPR + C::WPR - 2] : 0u;
+                    id = node_of(PF16[r * C::WPR + C::WPR - 1], word_starts<RUNS>(wl, wll), 31);
                 }
                 uint32_t x = id, p = P[id];
                 while (!(p & kRoot)) {
@@ -678,11 +697,11 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
             else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; }
             else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; }
             const int w = c >> 5, b = c & 31;
-            const uint32_t wm = M[r * C::WX + w];
+            const uint32_t wm = M[r * C::WPR + w];
             uint32_t v = kBG;
             if ((wm >> b) & 1u) {
-                const uint32_t wl = w > 0 ? M[r * C::WX + w - 1] : 0u;
-                const uint32_t code = T[node_of(PF16[r * C::WX + w], word_starts<RUNS>(wm, wl), uint32_t(b))];
+                const uint32_t wl = w > 0 ? M[r * C::WPR + w - 1] : 0u;
+                const uint32_t code = T[node_of(PF16[r * C::WPR + w], word_starts<RUNS>(wm, wl), uint32_t(b))];
                 if (code & kSeam) v = FR[1 + (code & kCode)];  // sides facing the image edge are not seams
             }
             wt[C::W_REC + i] = v;
@@ -812,8 +831,6 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
     }
     __syncthreads();
 
-    uint8_t* stg = smem + E::STG_OFF + warp * 4096;  // 32 x 32 u32, 128B-swizzled
-    uint8_t* myrow = stg + lane * 128;
     const int sw = lane & 7;
     uint32_t it = 0;
     TileWalk walk(blockIdx.x, G, g);
@@ -836,64 +853,70 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         const TileId ti = walk.cur;
         const uint32_t x0 = ti.tx * C::TW, y0 = ti.ty * C::TH;
 
-        const uint32_t m = M[row * C::WX + wx];
-        const uint32_t lm = wx > 0 ? M[row * C::WX + wx - 1] : 0u;
-        const uint32_t st = word_starts<RUNS>(m, lm);
-        const uint32_t pfx = PF16[row * C::WX + wx];
         auto lab_of = [&](uint32_t v) -> uint32_t {
             return (v & kSeam) ? FT[v & kCode] : pos_gidx<C>(v & kCode, x0, y0, g);
         };
-        if (TMA_ST) {  // this warp's previous TMA store must have read the staging tile
+        if (TMA_ST) {  // this warp's previous TMA stores must have read the staging tiles
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
         }
-        uint32_t cur = ((st & 1u) || !(m & 1u)) ? kBG : lab_of(TBL[pfx - 1]);  // run continuing from the left
-        {
-            const uint16_t* e = TBL + pfx;
-            uint32_t tt = st;
-            while (tt) {
-                const uint32_t b = __ffs(tt) - 1;
-                tt &= tt - 1;
-                *reinterpret_cast<uint32_t*>(myrow + ((((b >> 2) ^ sw) << 4) | ((b & 3) << 2))) = lab_of(*e++);
-            }
-        }
         uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            uint4* p = reinterpret_cast<uint4*>(myrow + ((c ^ sw) << 4));
-            uint4 v = *p;
-            uint32_t a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int i = 4 * c + q;
-                cur = ((st >> i) & 1u) ? a[q] : cur;
-                a[q] = ((m >> i) & 1u) ? cur : kBG;
+#pragma unroll 1
+        for (int k = 0; k < C::WPL; ++k) {  // this lane's row words, one 32x32 staging tile each
+            const int wc = wx * C::WPL + k;
+            uint8_t* stg = smem + E::STG_OFF + (warp * C::WPL + k) * 4096;  // 32 x 32 u32, 128B-swizzled
+            uint8_t* myrow = stg + lane * 128;
+            const uint32_t m = M[row * C::WPR + wc];
+            const uint32_t lm = wc > 0 ? M[row * C::WPR + wc - 1] : 0u;
+            const uint32_t st = word_starts<RUNS>(m, lm);
+            const uint32_t pfx = PF16[row * C::WPR + wc];
+            uint32_t cur = ((st & 1u) || !(m & 1u)) ? kBG : lab_of(TBL[pfx - 1]);  // run continuing from the left
+            {
+                const uint16_t* e = TBL + pfx;
+                uint32_t tt = st;
+                while (tt) {
+                    const uint32_t b = __ffs(tt) - 1;
+                    tt &= tt - 1;
+                    *reinterpret_cast<uint32_t*>(myrow + ((((b >> 2) ^ sw) << 4) | ((b & 3) << 2))) = lab_of(*e++);
+                }
             }
-            if (TMA_ST) {
-                *p = make_uint4(a[0], a[1], a[2], a[3]);
-            } else {
-                const uint32_t gy = y0 + row;
-                if (gy < g.H) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t gx = x0 + wx * 32 + 4 * c + q;
-                        if (gx < g.W) Lf[size_t(gy) * g.W + gx] = a[q];
+            for (int c = 0; c < 8; ++c) {
+                uint4* p = reinterpret_cast<uint4*>(myrow + ((c ^ sw) << 4));
+                uint4 v = *p;
+                uint32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = 4 * c + q;
+                    cur = ((st >> i) & 1u) ? a[q] : cur;
+                    a[q] = ((m >> i) & 1u) ? cur : kBG;
+                }
+                if (TMA_ST) {
+                    *p = make_uint4(a[0], a[1], a[2], a[3]);
+                } else {
+                    const uint32_t gy = y0 + row;
+                    if (gy < g.H) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t gx = x0 + wc * 32 + 4 * c + q;
+                            if (gx < g.W) Lf[size_t(gy) * g.W + gx] = a[q];
+                        }
                     }
                 }
             }
-        }
-        if (TMA_ST) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                if (CCL_HINTS)
-                    tma_store_3d_hint(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg,
-                                      policy_evict_first());  // OOB clipped; labels stream out
-                else
-                    tma_store_3d(&tm_lab, int(x0 + wx * 32), int(y0 + wy * 32), int(ti.fz), stg);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (TMA_ST) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CCL_HINTS)
+                        tma_store_3d_hint(&tm_lab, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg,
+                                          policy_evict_first());  // OOB clipped; labels stream out
+                    else
+                        tma_store_3d(&tm_lab, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg);
+                }
             }
         }
+        if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
         if (CCL_DISCARD) {  // this tile's hand-off data (work tile + its forest segment) is dead:
             // drop the dirty lines from L2 instead of writing them back
@@ -1026,10 +1049,10 @@ cudaError_t launch_local(const LaunchArgs& a) {
 
 template <bool RUNS>
 static cudaError_t launch_final_v(const LaunchArgs& a) {
-    using C = TileCfg;
+    using C = ECfg;
     using E = ELayout<C, RUNS>;
     const uint32_t nt = tile_count(a);
-    cudaError_t e = launch_pdl(k_resolve<C>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
+    cudaError_t e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
                                a.g, nt);
     if (e != cudaSuccess) return e;
     if (a.tma_store) {
