@@ -10,20 +10,11 @@
 #ifndef CCL_JUMP
 #define CCL_JUMP 1  // pointer-jumping rounds over the coarse forest in kernel (a)
 #endif
-#ifndef CCL_WAVE
-#define CCL_WAVE 0  // barrier between flatten waves in kernel (a)
-#endif
-#ifndef CCL_ILP
-#define CCL_ILP 1  // independent pointer walks per thread in kernel (a)'s node passes
-#endif
 #ifndef CCL_ULCAP
 #define CCL_ULCAP 128  // union-list entries per warp in kernel (a)
 #endif
 #ifndef CCL_HINTS
 #define CCL_HINTS 1  // L2 evict-first / evict-last policies on streams vs hand-off data
-#endif
-#ifndef CCL_DISCARD
-#define CCL_DISCARD 0  // kernel (e) discards consumed hand-off lines from L2
 #endif
 #ifndef CCL_PDL
 #define CCL_PDL 1  // programmatic dependent launch of kernels (d), (d2), (e)
@@ -31,26 +22,11 @@
 #ifndef CCL_SEAM_MATCH
 #define CCL_SEAM_MATCH 1  // kernel (d): one union per distinct local-root pair per warp
 #endif
-#ifndef CCL_COARSE2
-#define CCL_COARSE2 1  // kernel (a) coarse scan as two loops (root codes, then links)
-#endif
-#ifndef CCL_JUMPBAR
-#define CCL_JUMPBAR 0
-#endif
 #ifndef CCL_CARVEOUT
 #define CCL_CARVEOUT 100  // preferred shared-memory carveout (%) of kernels (a) and (e)
 #endif
 #ifndef CCL_EMINB
 #define CCL_EMINB 2
-#endif
-#ifndef CCL_ORDERED
-#define CCL_ORDERED 0  // kernel (a) node passes: contiguous id range per warp, in order
-#endif
-#ifndef CCL_L2PERSIST
-#define CCL_L2PERSIST 0  // persisting-L2 window over the work buffer for (a) and (e)
-#endif
-#ifndef CCL_TABLE_WAVES
-#define CCL_TABLE_WAVES 1  // barrier-separated waves of kernel (a)'s table pass
 #endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0

@@ -506,44 +506,14 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
 #pragma unroll 1
             for (int j = 0; j < CCL_JUMP; ++j) {
                 volatile node_t* vP = P;
-#if CCL_ORDERED
-                // each warp sweeps a contiguous id range in order (32 ids per
-                // step): a node's parent, one or two rows up, was usually jumped
-                // by this warp a step earlier, so the jumps compound
-                {
-                    const uint32_t chunk = ((nodes + C::NWARP - 1) / C::NWARP + 31) & ~31u;
-                    const uint32_t lo = warp * chunk, hi = min(lo + chunk, nodes);
-                    for (uint32_t base = lo; base < hi; base += 32) {
-                        const uint32_t id = base + lane;
-                        if (id < hi) {
-                            const uint32_t p = vP[id];
-                            const uint32_t pp = (p & kRoot) ? p : vP[p];
-                            if (!(pp & kRoot)) vP[id] = node_t(pp);
-                        }
-                        __syncwarp();
-                    }
+                for (uint32_t id = tid; id < nodes; id += C::NT) {
+                    const uint32_t p = vP[id];
+                    const uint32_t pp = (p & kRoot) ? p : vP[p];
+                    if (!(pp & kRoot)) vP[id] = node_t(pp);
                 }
-#else
-                // CCL_ILP independent nodes per thread in flight (latency-bound pass)
-                for (uint32_t base = tid; base < nodes; base += CCL_ILP * C::NT) {
-                    uint32_t p[CCL_ILP], pp[CCL_ILP];
-#pragma unroll
-                    for (int k = 0; k < CCL_ILP; ++k) {
-                        const uint32_t id = base + k * C::NT;
-                        p[k] = id < nodes ? vP[id] : kRoot;
-                    }
-#pragma unroll
-                    for (int k = 0; k < CCL_ILP; ++k) pp[k] = (p[k] & kRoot) ? p[k] : vP[p[k]];
-#pragma unroll
-                    for (int k = 0; k < CCL_ILP; ++k) {
-                        const uint32_t id = base + k * C::NT;
-                        if (id < nodes && !(pp[k] & kRoot)) vP[id] = node_t(pp[k]);
-                    }
-                }
-#endif
                 // no barrier after the last round: jumps and unions only ever
                 // replace an entry by an ancestor, and unions CAS root entries only
-                if (j + 1 < CCL_JUMP || CCL_JUMPBAR) __syncthreads();
+                if (j + 1 < CCL_JUMP) __syncthreads();
                 CCL_PH(3);
             }
         }
@@ -633,43 +603,15 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         // already rewritten (parents always have smaller ids) end walks early.
         {
             volatile node_t* vP = P;
-#if CCL_ORDERED
-            // contiguous id range per warp, in order: parents one or two rows up
-            // were rewritten by this warp a step or two earlier, so most walks
-            // take one hop
-            const uint32_t chunk = ((nodes + C::NWARP - 1) / C::NWARP + 31) & ~31u;
-            const uint32_t lo = warp * chunk, hi = min(lo + chunk, nodes);
-            for (uint32_t base = lo; base < hi; base += 32) {
-                const uint32_t id = base + lane;
-                if (id < hi) {
-                    uint32_t p = vP[id];
-                    if (!(p & kRoot)) {
-                        do {
-                            p = vP[p];
-                        } while (!(p & kRoot));
-                        vP[id] = node_t(p);
-                    }
-                }
-                __syncwarp();
-            }
-#else
-            // CCL_TABLE_WAVES waves of ids with a barrier between them: walks in
-            // a later wave stop at the already rewritten nodes of earlier waves
-            for (int wv = 0; wv < CCL_TABLE_WAVES; ++wv) {
-                const uint32_t lo = uint32_t((uint64_t(nodes) * wv) / CCL_TABLE_WAVES);
-                const uint32_t hi = uint32_t((uint64_t(nodes) * (wv + 1)) / CCL_TABLE_WAVES);
-                if (wv) __syncthreads();
-                for (uint32_t id = lo + tid; id < hi; id += C::NT) {
-                    uint32_t p = vP[id];
-                    if (!(p & kRoot)) {
-                        do {
-                            p = vP[p];
-                        } while (!(p & kRoot));
-                        vP[id] = node_t(p);
-                    }
+            for (uint32_t id = tid; id < nodes; id += C::NT) {
+                uint32_t p = vP[id];
+                if (!(p & kRoot)) {
+                    do {
+                        p = vP[p];
+                    } while (!(p & kRoot));
+                    vP[id] = node_t(p);
                 }
             }
-#endif
         }
         const uint32_t nf = FR[0];
         if (tid == 0) {
@@ -918,14 +860,6 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         }
         if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
-        if (CCL_DISCARD) {  // this tile's hand-off data (work tile + its forest segment) is dead:
-            // drop the dirty lines from L2 instead of writing them back
-            const uint8_t* base = reinterpret_cast<const uint8_t*>(work_tile<C>(const_cast<uint32_t*>(work), t));
-            for (int i = tid; i < C::TILE_WORDS / 32; i += C::NT) discard_l2(base + 128 * i);
-            const uint8_t* fb = reinterpret_cast<const uint8_t*>(work + size_t(ntiles) * C::TILE_WORDS +
-                                                                 size_t(t) * 2 * C::MAXF);
-            for (int i = tid; i < 2 * C::MAXF / 32; i += C::NT) discard_l2(fb + 128 * i);
-        }
     }
     if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -963,57 +897,26 @@ static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntil
 }
 
 static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
-static size_t work_bytes_used(const LaunchArgs& a) {
-    return size_t(tile_count(a)) * (size_t(TileCfg::TILE_WORDS) + 2 * size_t(TileCfg::MAXF)) * 4;
-}
 
-// Launch with programmatic stream serialization (the kernel calls pdl_wait()
-// before reading what the previous kernel in the stream produced) and, with
-// CCL_L2PERSIST, a persisting-L2 access-policy window over the work buffer
-// (the hand-off between the kernels).
+// Launch (optionally) with programmatic stream serialization: the kernel calls
+// pdl_wait() before reading what the previous kernel in the stream produced.
 template <class K, class... Args>
-static cudaError_t launch_ex(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, bool pdl, void* win,
-                             size_t win_bytes, Args... args) {
+static cudaError_t launch_ex(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, bool pdl, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    int n = 0;
-    if (pdl) {
-        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[n++].val.programmaticStreamSerializationAllowed = CCL_PDL;
-    }
-#if CCL_L2PERSIST
-    if (win && win_bytes) {
-        static int max_win = -1, max_persist = -1;
-        if (max_win < 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(max_persist));
-        }
-        const size_t nb = win_bytes < size_t(max_win) ? win_bytes : size_t(max_win);
-        attr[n].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[n].val.accessPolicyWindow.base_ptr = win;
-        attr[n].val.accessPolicyWindow.num_bytes = nb;
-        attr[n].val.accessPolicyWindow.hitRatio = nb ? float(double(max_persist) / double(nb) > 1.0 ? 1.0 : double(max_persist) / double(nb)) : 0.f;
-        attr[n].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[n++].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    }
-#else
-    (void)win;
-    (void)win_bytes;
-#endif
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = CCL_PDL;
     cfg.attrs = attr;
-    cfg.numAttrs = n;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 template <class K, class... Args>
 static cudaError_t launch_pdl(K kernel, dim3 grid, int threads, int smem, cudaStream_t s, Args... args) {
-    return launch_ex(kernel, grid, threads, smem, s, true, nullptr, 0, args...);
+    return launch_ex(kernel, grid, threads, smem, s, true, args...);
 }
 
 template <int VAR>
@@ -1026,8 +929,7 @@ static cudaError_t launch_local_v(const LaunchArgs& a) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
         const cudaError_t e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, VAR)), C::NT, A::SMEM,
-                                        a.stream, false, a.work, work_bytes_used(a), a.tm_img, a.img, a.labels,
-                                        a.work, a.g, nt);
+                                        a.stream, false, a.tm_img, a.img, a.labels, a.work, a.g, nt);
         if (e != cudaSuccess) return e;
     } else {
         auto k = k_local<C, VAR, false>;
@@ -1059,9 +961,8 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
         auto k = k_final<C, RUNS, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_ex(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
-                      true, a.work, work_bytes_used(a), a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g,
-                      nt);
+        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
+                       a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
         auto k = k_final<C, RUNS, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
