@@ -94,7 +94,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
  *                             identically on every strip (no broadcast), then
  *                             each own seam root's final label is written into
  *                             the strip's compact forest (in d_work)
- *   5. ccl_strip_final        kernel (e) on the strip
+ *   5. ccl_strip_final        kernel (e) on the strip (same variant as step 1)
  * Steps 2-4 must all run before step 5; d_work (the strip's work buffer from
  * step 1) carries the forest between the steps, and the label buffer is
  * scratch until step 5 writes it. */
@@ -108,7 +108,7 @@ ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint
                                   uint32_t strip_index, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
                                   uint32_t* d_labels, void* d_work, uint32_t* d_scratch, void* stream);
 ccl_status ccl_strip_final(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h,
-                           uint32_t* d_labels, const void* d_work, void* stream);
+                           uint32_t* d_labels, const void* d_work, int variant, void* stream);
 /* d_scratch for ccl_strip_seam_resolve must hold ccl_strip_scratch_words(n_strips, w) u32;
  * d_work (kernel (a) -> kernel (e) hand-off: per-tile masks, run table and
  * seam-root list) must hold ccl_work_bytes(w, h, 1) bytes and stay untouched

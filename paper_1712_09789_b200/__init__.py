@@ -77,7 +77,7 @@ _sig("ccl_label_batch", _c, _vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _c, _vp)
 _sig("ccl_strip_local", _c, _vp, _vp, _sz, _u32, _u32, _u32, _u32, _vp, _vp, _c, _vp)
 _sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
 _sig("ccl_strip_seam_resolve", _c, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
-_sig("ccl_strip_final", _c, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp)
+_sig("ccl_strip_final", _c, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _c, _vp)
 _sig("ccl_strip_scratch_words", _sz, _u32, _u32)
 _sig("ccl_gen_random_device", _c, _vp, _vp, _u32, _u32, _u32, ctypes.c_double, ctypes.c_uint64, _vp)
 _sig("ccl_label_to_cclm", _c, _vp, _u8p, _u32, _u32, _c, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64))

@@ -359,14 +359,17 @@ ccl_status ccl_strip_seam_resolve(ccl_ctx* ctx, const uint32_t* d_seam_all, uint
 }
 
 ccl_status ccl_strip_final(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, uint32_t full_h, uint32_t* d_labels,
-                           const void* d_work, void* stream) {
+                           const void* d_work, int variant, void* stream) {
     if (!ctx || !d_labels || !d_work) return fail(CCL_EINVAL, "null argument");
     DeviceGuard dg(ctx->device);
     cclk::LaunchArgs a{};
     if (ccl_status s = strip_geo(w, h, row0, full_h, w, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // kernel (e) never reads the image; any 16B-aligned pointer satisfies prepare()
-    if (ccl_status s = prepare(&a, reinterpret_cast<const uint8_t*>(d_work), 16, 16 * size_t(h), 1, d_labels, 0, st))
+    // kernel (e) never reads the image; any 16B-aligned pointer satisfies prepare().
+    // `variant` must be the one ccl_strip_local used: it selects the node
+    // layout kernel (e) expands (band runs, row runs or pixels).
+    if (ccl_status s =
+            prepare(&a, reinterpret_cast<const uint8_t*>(d_work), 16, 16 * size_t(h), 1, d_labels, variant, st))
         return s;
     a.work = static_cast<uint32_t*>(const_cast<void*>(d_work));
     CCL_CHECK(cclk::launch_final(a));

@@ -28,6 +28,15 @@
 #ifndef CCL_EMINB
 #define CCL_EMINB 2
 #endif
+#ifndef CCL_BAND
+#define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
+#endif
+#ifndef CCL_BWPL
+#define CCL_BWPL 1  // 32-px row words per lane in the band kernel (a)
+#endif
+#ifndef CCL_BMINB
+#define CCL_BMINB 10  // min resident CTAs of the band kernel (a)
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif

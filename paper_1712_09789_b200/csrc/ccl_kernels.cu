@@ -32,17 +32,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ccl_device.cuh"
 #include "ccl_internal.h"
 
 namespace cclk {
 
-template <int WX_, int WY_, int WPL_ = 1>
+template <int WX_, int WY_, int WPL_ = 1, int RPL_ = 1>
 struct Cfg {
     static constexpr int WX = WX_, WY = WY_;  // warps across / down the tile
     static constexpr int WPL = WPL_;          // 32-px row words per lane
+    static constexpr int RPL = RPL_;          // rows per lane (2: a lane owns a 2-row band)
     static constexpr int WPR = WX * WPL;      // row words per tile row
-    static constexpr int TW = 32 * WPR, TH = 32 * WY, NT = 32 * WX * WY, NWARP = WX * WY;
+    static constexpr int TW = 32 * WPR, TH = 32 * RPL * WY, NT = 32 * WX * WY, NWARP = WX * WY;
     static constexpr int PX = TW * TH;
     static constexpr int MAXF = 2 * TW + 2 * TH;  // bound on seam-touching roots (one per boundary run)
     // work buffer (global) per tile, in u32 words:
@@ -53,12 +56,15 @@ struct Cfg {
     static constexpr int W_HEAD = 0;
     static constexpr int W_MASK = 4;
     static constexpr int W_PF = W_MASK + MW;
-    static constexpr int W_LIST = W_PF + MW / 2;
+    static constexpr int BSW = (TH / 2) * WPR;  // band-start words (band kernel (a) only)
+    static constexpr int W_BS = W_PF + MW / 2;
+    static constexpr int W_LIST = W_BS + BSW;
     static constexpr int W_REC = W_LIST + MAXF;
     static constexpr int W_TBL = W_REC + 2 * TW + 2 * TH;
     static constexpr int TILE_WORDS = (W_TBL + PX / 2 + 31) / 32 * 32;  // table sized for pixel nodes; 128B lines
     static_assert((2 * MAXF) % 32 == 0, "per-tile forest segments are whole 128B lines");
-    static constexpr int S1_BYTES = (W_LIST - W_HEAD) * 4;  // head + masks + prefixes: one bulk copy
+    static constexpr int S1_BYTES = (W_BS - W_HEAD) * 4;         // head + masks + prefixes: one copy
+    static constexpr int S1_BYTES_BAND = (W_LIST - W_HEAD) * 4;  // ... + band starts (band kernel (a))
     // After the tiles: the COMPACT global forest, one {parent, key} u32 pair per
     // possible seam-touching root (node n = tile * MAXF + rank, key = the root's
     // global raster index), then the strip-mode area (edge rows + their roots).
@@ -72,18 +78,25 @@ struct Cfg {
 // tile (one 32-px word per lane): same TW, TH, MW, MAXF, hence the same work tile.
 using TileCfg = Cfg<CCL_TILE_WX, CCL_TILE_WY, CCL_WPL>;
 using ECfg = Cfg<CCL_TILE_WX * CCL_WPL, CCL_TILE_WY, 1>;
+// 2-row band kernels: (a) lane = band with CCL_BWPL words; (e) lane = band, one word.
+using BandCfg = Cfg<TileCfg::WPR / CCL_BWPL, TileCfg::TH / 64, CCL_BWPL, 2>;
+using BandECfg = Cfg<TileCfg::WPR, TileCfg::TH / 64, 1, 2>;
+static_assert(BandCfg::TW == TileCfg::TW && BandCfg::TH == TileCfg::TH && BandCfg::TILE_WORDS == TileCfg::TILE_WORDS,
+              "band kernel (a) writes the same work tiles");
+static_assert(BandECfg::TILE_WORDS == TileCfg::TILE_WORDS, "band kernel (e) reads the same work tiles");
 static_assert(ECfg::TW == TileCfg::TW && ECfg::TH == TileCfg::TH && ECfg::TILE_WORDS == TileCfg::TILE_WORDS,
               "kernel (e) must see kernel (a)'s work tiles");
 
 // Kernel (a) shared memory, per node granularity (runs: <= PX/2 nodes).
-template <class C, bool RUNS>
+template <class C, bool RUNS, bool BAND = false>
 struct ALayout {
     static constexpr int MAXN = RUNS ? C::PX / 2 : C::PX;
     static constexpr int P_OFF = 0;                                        // u16 parents / root codes, then the table
     static constexpr int FB_OFF = P_OFF + MAXN * 2;                        // seam-root bitmap
     static constexpr int M_OFF = FB_OFF + ((MAXN / 32 * 4 + 127) / 128) * 128;  // row-word masks
     static constexpr int PF16_OFF = M_OFF + C::MW * 4;                     // u16 prefixes (contiguous: one bulk store)
-    static constexpr int PF_OFF = PF16_OFF + C::MW * 2;                    // u32 counts / prefixes
+    static constexpr int BS_OFF = PF16_OFF + C::MW * 2;                    // band starts (band kernel)
+    static constexpr int PF_OFF = BS_OFF + (BAND ? C::BSW * 4 : 0);        // u32 counts / prefixes
     static constexpr int BT_OFF = PF_OFF + C::MW * 4;                      // band totals (+ total)
     static constexpr int FR_OFF = BT_OFF + 128;                            // [count, global idx of seam roots]
     static constexpr int UL_CAP = CCL_ULCAP;                               // union pairs per warp
@@ -94,15 +107,16 @@ struct ALayout {
 };
 
 // Kernel (e) shared memory: 3 head/mask stages, 2 table/label stages, staging.
-template <class C, bool RUNS>
+template <class C, bool RUNS, bool BAND = false>
 struct ELayout {
-    static constexpr int S1 = (C::S1_BYTES + 127) / 128 * 128;
+    static constexpr int S1B = BAND ? C::S1_BYTES_BAND : C::S1_BYTES;
+    static constexpr int S1 = (S1B + 127) / 128 * 128;
     static constexpr int TBLB = RUNS ? C::PX : 2 * C::PX;                 // u16 node table
     static constexpr int S2 = (C::MAXF * 4 + TBLB + 127) / 128 * 128;     // resolved labels + table
     static constexpr int S1_OFF = 0;
     static constexpr int S2_OFF = S1_OFF + 3 * S1;
     static constexpr int STG_OFF = ((S2_OFF + 2 * S2) + 1023) / 1024 * 1024;
-    static constexpr int BAR_OFF = STG_OFF + C::NWARP * C::WPL * 4096;
+    static constexpr int BAR_OFF = STG_OFF + C::NWARP * C::WPL * C::RPL * 4096;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;
 };
 
@@ -660,6 +674,376 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     pdl_trigger();
 }
 
+// ------------------------------------------------------------------ kernel (a), 2-row bands (C2FL)
+// Same phases as k_local, on 2-row BAND RUNS instead of row runs: within rows
+// (2b, 2b+1) the 4-connected pieces are column intervals where every column
+// has a foreground pixel and consecutive columns share a foreground row
+// (lk = t & t>>1 | u & u>>1), so a band run's start mask is pure bit work and
+// the prefix / node_of machinery carries over unchanged with about half the
+// nodes of row runs (at d = 0.5).  A band run's minimum pixel -- its code when
+// it is a root -- is its first top-row pixel, else its first column in the
+// bottom row; node ids are not in code order inside a band, so unions compare
+// root codes (the class root is the node of the component's minimum pixel,
+// forest.hpp:98-111 restated on positions).  Lane = band, one word per lane.
+__device__ __forceinline__ uint32_t band_starts(uint32_t t, uint32_t u, uint32_t tl, uint32_t ul) {
+    const uint32_t lk = (t & (t >> 1)) | (u & (u >> 1));          // column c linked to c + 1
+    const uint32_t cl = (((tl >> 31) & t) | ((ul >> 31) & u)) & 1u;  // bit 0 linked to the word on the left
+    return (t | u) & ~((lk << 1) | cl);
+}
+template <class C>
+__device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, int w) {
+    const uint32_t t = M[(2 * band) * C::WPR + w], u = M[(2 * band + 1) * C::WPR + w];
+    const uint32_t tl = w > 0 ? M[(2 * band) * C::WPR + w - 1] : 0u, ul = w > 0 ? M[(2 * band + 1) * C::WPR + w - 1] : 0u;
+    return band_starts(t, u, tl, ul);
+}
+// Min-union on root codes (positions): the root whose code is larger is
+// linked below the other with a CAS on its entry.
+__device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b) {
+    volatile node_t* vP = P;
+    for (;;) {
+        a = nfind(P, a);
+        b = nfind(P, b);
+        if (a == b) return;
+        uint32_t ca = vP[a], cb = vP[b];
+        if (!(ca & kRoot) || !(cb & kRoot)) continue;  // linked meanwhile: find again
+        if ((ca & kCode) < (cb & kCode)) {
+            const uint32_t t = a; a = b; b = t;
+            const uint32_t tc = ca; ca = cb; cb = tc;
+        }
+        if (atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(ca),
+                      static_cast<unsigned short>(b)) == ca)
+            return;
+    }
+}
+
+template <class C, bool TMA>
+__global__ void __launch_bounds__(C::NT, CCL_BMINB)
+    k_local_band(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img, uint32_t* work, Geo g,
+                 uint32_t ntiles) {
+    static_assert(C::RPL == 2, "lane = 2-row band");
+    using A = ALayout<C, true, true>;
+    constexpr int WPL = C::WPL, WPR = C::WPR;
+    uint8_t* smem = aligned_smem();
+    node_t* P = reinterpret_cast<node_t*>(smem + A::P_OFF);
+    uint32_t* FB = reinterpret_cast<uint32_t*>(smem + A::FB_OFF);
+    uint32_t* M = reinterpret_cast<uint32_t*>(smem + A::M_OFF);
+    uint16_t* PF16 = reinterpret_cast<uint16_t*>(smem + A::PF16_OFF);  // per (band, word)
+    uint32_t* BS = reinterpret_cast<uint32_t*>(smem + A::BS_OFF);      // band starts per (band, word)
+    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::PF_OFF);
+    uint32_t* BT = reinterpret_cast<uint32_t*>(smem + A::BT_OFF);
+    uint32_t* FR = reinterpret_cast<uint32_t*>(smem + A::FR_OFF);
+    uint8_t* IMG = smem + A::IMG_OFF;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wx = warp % C::WX, wy = warp / C::WX;
+    const int band = wy * 32 + lane;  // rows 2*band, 2*band + 1
+    const int r0 = 2 * band, r1 = r0 + 1;
+    const int wc0 = wx * WPL;         // first word column of this lane
+    const Forest fst = forest_of<C>(work, ntiles);
+    uint32_t* SE = strip_area<C>(work, ntiles);
+
+    auto issue_at = [&](const TileId& q) {
+        mbar_expect_tx(bar, C::PX);
+        tma_load_3d_hint(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar, policy_evict_first());
+    };
+    if (TMA && tid == 0) {
+        prefetch_tmap(&tm_img);
+        mbar_init(bar, 1);
+        if (blockIdx.x < ntiles) issue_at(tile_of(blockIdx.x, g));
+    }
+    // node of the pixel (r, c) of a tile (the pixel must be foreground)
+    auto node_px = [&](int r, int c) -> uint32_t {
+        const int w = c >> 5;
+        return node_of(PF16[(r >> 1) * WPR + w], BS[(r >> 1) * WPR + w], uint32_t(c & 31));
+    };
+
+    uint32_t it = 0;
+    TileWalk walk(blockIdx.x, gridDim.x, g);
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
+        const TileId ti = walk.cur;
+        const uint32_t tx = ti.tx, ty = ti.ty;
+        const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
+        uint32_t* wt = work_tile<C>(work, t);
+
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        for (int i = tid; i < A::MAXN / 32; i += C::NT) FB[i] = 0u;
+        if (tid == 0) FR[0] = 0u;
+
+        // ---- row-word foreground masks (byte == 1)
+        if (TMA) {
+            mbar_wait(bar, it & 1u);
+            constexpr int CPR = C::TW / 16;
+            uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
+#pragma unroll
+            for (int c = tid; c < C::TH * CPR; c += C::NT) {
+                const uint4 q = *reinterpret_cast<const uint4*>(IMG + c * 16);
+                M16[c] = static_cast<uint16_t>(eq1_mask16(q));
+            }
+        } else {  // unaligned pitch: byte loads, one mask word per thread and step
+            for (int i = tid; i < C::MW; i += C::NT) {
+                const int r = i / WPR, w = i - r * WPR;
+                const uint32_t gy = y0 + r;
+                uint32_t mm = 0u;
+                if (gy < g.H) {
+                    const uint8_t* src = img + size_t(ti.fz) * g.frame_pitch + size_t(gy) * g.img_pitch;
+                    for (int b = 0; b < 32; ++b) {
+                        const uint32_t gx = x0 + 32 * w + b;
+                        if (gx < g.W && src[gx] == 1) mm |= 1u << b;
+                    }
+                }
+                M[i] = mm;
+            }
+        }
+        __syncthreads();
+        if (TMA && tid == 0 && t + gridDim.x < ntiles) {
+            TileWalk nx = walk;
+            nx.advance();
+            issue_at(nx.cur);
+        }
+
+        // ---- band runs of this lane's words: coarse row scan in raster (band, word) order
+        uint32_t tm[WPL], um[WPL], bs[WPL], ul0;
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int wc = wc0 + k;
+            tm[k] = M[r0 * WPR + wc];
+            um[k] = M[r1 * WPR + wc];
+            const uint32_t tl = k > 0 ? tm[k - 1] : (wc > 0 ? M[r0 * WPR + wc - 1] : 0u);
+            const uint32_t ul = k > 0 ? um[k - 1] : (wc > 0 ? M[r1 * WPR + wc - 1] : 0u);
+            if (k == 0) ul0 = ul;
+            bs[k] = band_starts(tm[k], um[k], tl, ul);
+            cnt += __popc(bs[k]);
+        }
+        uint32_t nodes;
+        const uint32_t pfx0 = tile_prefix<C>(cnt, CNT, BT, band, wx, wy, lane, &nodes);
+        uint32_t pfx[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            pfx[k] = k > 0 ? pfx[k - 1] + __popc(bs[k - 1]) : pfx0;
+            PF16[band * WPR + wc0 + k] = uint16_t(pfx[k]);
+            BS[band * WPR + wc0 + k] = bs[k];
+        }
+        if (C::WY > 1) __syncthreads();  // lane 0 of a lower warp row reads the band above from smem
+        // the band above (lane - 1, or the warp row above): bottom row, starts, prefixes
+        uint32_t ua[WPL], ubs[WPL], upfx[WPL], ual0;
+        {
+            const uint32_t ual_sh = __shfl_up_sync(0xffffffffu, ul0, 1);
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) {
+                ua[k] = __shfl_up_sync(0xffffffffu, um[k], 1);
+                ubs[k] = __shfl_up_sync(0xffffffffu, bs[k], 1);
+                upfx[k] = __shfl_up_sync(0xffffffffu, pfx[k], 1);
+            }
+            ual0 = ual_sh;
+            if (lane == 0) {
+                if (band == 0) {  // the tile's top side: a seam, handled by kernel (d)
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) ua[k] = ubs[k] = upfx[k] = 0u;
+                    ual0 = 0u;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) {
+                        ua[k] = M[(r0 - 1) * WPR + wc0 + k];
+                        ubs[k] = BS[(band - 1) * WPR + wc0 + k];
+                        upfx[k] = PF16[(band - 1) * WPR + wc0 + k];
+                    }
+                    ual0 = wc0 > 0 ? M[(r0 - 1) * WPR + wc0 - 1] : 0u;
+                }
+            }
+        }
+
+        // ---- init + coarse column scan: each band run links to the band run
+        // above that holds its first overlap in its word (plain stores); a root
+        // band run carries its minimum pixel as its code
+        uint32_t U[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int wc = wc0 + k;
+            const uint32_t tl = k > 0 ? tm[k - 1] : (wc > 0 ? M[r0 * WPR + wc - 1] : 0u);
+            const uint32_t ual = k > 0 ? ua[k - 1] : ual0;
+            const uint32_t o = tm[k] & ua[k];
+            const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
+            const uint32_t os = (o & ~(o << 1)) & ~ocont;
+            uint32_t firstm = 0u;
+            uint32_t tt = bs[k], id = pfx[k];
+            const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
+            while (tt) {
+                const uint32_t a = __ffs(tt) - 1;
+                tt &= tt - 1;
+                const uint32_t nx = tt ? __ffs(tt) - 1 : 32u;
+                const uint32_t span = (0xFFFFFFFFu << a) & (nx < 32 ? ~(0xFFFFFFFFu << nx) : 0xFFFFFFFFu);
+                const uint32_t ov = o & span;
+                uint32_t v;
+                if (ov) {
+                    const uint32_t f = __ffs(ov) - 1;
+                    firstm |= 1u << f;
+                    v = node_of(upfx[k], ubs[k], f);
+                } else {
+                    const uint32_t tb = tm[k] & span;
+                    if (tb) {
+                        v = kRoot | (rowpos0 + __ffs(tb) - 1);
+                    } else {
+                        uint32_t pos = rowpos1 + a;  // no top-row pixel in this word's part
+                        if (nx == 32) {              // the run may continue: look for a later top-row pixel
+                            for (int w = wc + 1; w < WPR; ++w) {
+                                const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
+                                const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
+                                const uint32_t below = bw ? (1u << (__ffs(bw) - 1)) - 1u : 0xFFFFFFFFu;
+                                const uint32_t cont = (tw | uw) & below;  // the part continuing from the left
+                                const uint32_t tc = tw & cont;
+                                if (tc) {
+                                    pos = uint32_t(r0 * C::TW + 32 * w) + __ffs(tc) - 1;
+                                    break;
+                                }
+                                if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
+                            }
+                        }
+                        v = kRoot | pos;
+                    }
+                }
+                P[id++] = node_t(v);
+            }
+            U[k] = os & ~firstm;  // remaining overlaps
+        }
+        // remaining overlaps -> this warp's union list
+        uint32_t* UL = reinterpret_cast<uint32_t*>(smem + A::UL_OFF) + warp * A::UL_CAP;
+        uint32_t nul;
+        {
+            uint32_t cu = 0;
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) cu += __popc(U[k]);
+            uint32_t inc = cu;
+#pragma unroll
+            for (int j = 1; j < 32; j <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, j);
+                if (lane >= j) inc += y;
+            }
+            const bool fits = inc <= uint32_t(A::UL_CAP);
+            nul = __reduce_max_sync(0xffffffffu, fits ? inc : 0u);
+            if (fits) {
+                uint32_t* dst = UL + (inc - cu);
+#pragma unroll
+                for (int k = 0; k < WPL; ++k) {
+                    while (U[k]) {
+                        const uint32_t b = __ffs(U[k]) - 1;
+                        U[k] &= U[k] - 1;
+                        *dst++ = node_of(pfx[k], bs[k], b) | (node_of(upfx[k], ubs[k], b) << 16);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- one pointer-jump round (no barrier after it: jumps and unions only
+        // replace an entry by an ancestor, unions CAS root entries only)
+        {
+            volatile node_t* vP = P;
+            for (uint32_t id = tid; id < nodes; id += C::NT) {
+                const uint32_t p = vP[id];
+                const uint32_t pp = (p & kRoot) ? p : vP[p];
+                if (!(pp & kRoot)) vP[id] = node_t(pp);
+            }
+        }
+        // ---- refinement unions on root codes
+        for (uint32_t k = lane; k < nul; k += 32) {
+            const uint32_t pr = UL[k];
+            nunion_pos(P, pr & 0xFFFFu, pr >> 16);
+        }
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            while (U[k]) {  // pairs that did not fit in the list
+                const uint32_t b = __ffs(U[k]) - 1;
+                U[k] &= U[k] - 1;
+                nunion_pos(P, node_of(pfx[k], bs[k], b), node_of(upfx[k], ubs[k], b));
+            }
+        }
+        __syncthreads();
+
+        // ---- seam-touching roots: every foreground pixel on a side facing a
+        // neighbour tile / strip marks its root once (balanced over threads)
+        const bool has_top = ty > 0 || g.edge_above;
+        const bool has_bot = ty + 1 < g.nty || g.edge_below;
+        const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
+        for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
+            int r, c;
+            bool act;
+            if (i < C::TW) { r = 0; c = i; act = has_top; }
+            else if (i < 2 * C::TW) { r = C::TH - 1; c = i - C::TW; act = has_bot; }
+            else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; act = has_left; }
+            else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; act = has_right; }
+            if (!act || !((M[r * WPR + (c >> 5)] >> (c & 31)) & 1u)) continue;
+            uint32_t x = node_px(r, c), p = P[x];
+            while (!(p & kRoot)) {
+                x = p;
+                p = P[x];
+            }
+            const uint32_t bit = 1u << (x & 31);
+            if (!(atomicOr(&FB[x >> 5], bit) & bit)) {
+                const uint32_t k = atomicAdd(FR, 1u);
+                const uint32_t n = t * uint32_t(C::MAXF) + k;
+                fst.f[2 * size_t(n)] = n;
+                fst.f[2 * size_t(n) + 1] = pos_gidx<C>(p & kCode, x0, y0, g);
+                FR[1 + k] = n;
+                P[x] = node_t(kRoot | kSeam | k);
+            }
+        }
+        __syncthreads();
+
+        // ---- node table: every entry becomes its root's code
+        {
+            volatile node_t* vP = P;
+            for (uint32_t id = tid; id < nodes; id += C::NT) {
+                uint32_t p = vP[id];
+                if (!(p & kRoot)) {
+                    do {
+                        p = vP[p];
+                    } while (!(p & kRoot));
+                    vP[id] = node_t(p);
+                }
+            }
+        }
+        const uint32_t nf = FR[0];
+        if (tid == 0) {
+            wt[C::W_HEAD + 0] = nf;
+            wt[C::W_HEAD + 1] = nodes;
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const uint64_t keep = policy_evict_last();
+            bulk_store_hint(wt + C::W_MASK, M, C::MW * 6 + C::BSW * 4, keep);  // row masks, band prefixes, band starts
+            if (nodes) bulk_store_hint(wt + C::W_TBL, P, (nodes * 2 + 15) & ~15u, keep);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+
+        // ---- seam records + strip-edge rows
+        for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
+            int r, c;
+            if (i < C::TW) { r = 0; c = i; }
+            else if (i < 2 * C::TW) { r = C::TH - 1; c = i - C::TW; }
+            else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; }
+            else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; }
+            uint32_t v = kBG;
+            if ((M[r * WPR + (c >> 5)] >> (c & 31)) & 1u) {
+                const uint32_t code = P[node_px(r, c)];
+                if (code & kSeam) v = FR[1 + (code & kCode)];
+            }
+            wt[C::W_REC + i] = v;
+            if (i < 2 * C::TW) {
+                const bool top = i < C::TW;
+                const bool edge = top ? (ty == 0 && g.edge_above) : (ty + 1 == g.nty && g.edge_below);
+                const uint32_t gx = x0 + c;
+                if (edge && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    pdl_trigger();
+}
+
 // ------------------------------------------------------------------ kernel (d)
 // Algorithm 2 over the compact seam records: one warp per 32 pixel pairs of a
 // tile seam (coalesced record loads); a pair whose predecessor along the seam
@@ -734,10 +1118,10 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
 // in flight (bulk copies).  Each warp expands its 32x32 block into a 128B-
 // swizzled staging tile and writes it with one TMA store: every label is
 // written exactly once and the image is never re-read.
-template <class C, bool RUNS, bool TMA_ST>
+template <class C, bool RUNS, bool TMA_ST, bool BAND>
 __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
                                                     const uint32_t* work, Geo g, uint32_t ntiles) {
-    using E = ELayout<C, RUNS>;
+    using E = ELayout<C, RUNS, BAND>;
     uint8_t* smem = aligned_smem();
     uint64_t* b1 = reinterpret_cast<uint64_t*>(smem + E::BAR_OFF);
     uint64_t* b2 = b1 + 3;
@@ -748,8 +1132,8 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
     auto s1buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S1_OFF + j * E::S1); };
     auto s2buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S2_OFF + j * E::S2); };
     auto s1 = [&](uint32_t t, uint32_t j) {
-        mbar_expect_tx(&b1[j], C::S1_BYTES);
-        bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), C::S1_BYTES, &b1[j]);
+        mbar_expect_tx(&b1[j], E::S1B);
+        bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), E::S1B, &b1[j]);
     };
     auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
         const uint32_t lb = (head[0] * 4 + 15) & ~15u, tb = (head[1] * 2 + 15) & ~15u;
@@ -790,6 +1174,7 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         mbar_wait(&b2[j2], (it >> 1) & 1u);
         const uint32_t* M = s1buf(j1) + 4;
         const uint16_t* PF16 = reinterpret_cast<const uint16_t*>(M + C::MW);
+        const uint32_t* BSt = M + C::MW + C::MW / 2;  // band starts (band mode)
         const uint32_t* FT = s2buf(j2);
         const uint16_t* TBL = reinterpret_cast<const uint16_t*>(FT + C::MAXF);
         const TileId ti = walk.cur;
@@ -803,16 +1188,87 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
             __syncwarp();
         }
         uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;
+        if constexpr (C::RPL == 2) {
+            // lane = band (rows 2b, 2b+1) of word column wx: the band starts are
+            // walked once and both rows are filled (two 32x32 staging tiles per warp)
+            const int b = wy * 32 + lane, wc = wx;
+            const int r0 = 2 * b, r1 = r0 + 1;
+            const int k = (r0 >> 5) & 1;  // staging tile of both rows (this warp covers rows 64 wy .. 64 wy + 63)
+            uint8_t* stg = smem + E::STG_OFF + (warp * 2 + k) * 4096;
+            uint8_t* row0 = stg + (r0 & 31) * 128;
+            uint8_t* row1 = stg + (r1 & 31) * 128;
+            const int sw0 = r0 & 7, sw1 = r1 & 7;
+            const uint32_t tm = M[r0 * C::WPR + wc], um = M[r1 * C::WPR + wc];
+            const uint32_t st = BSt[b * C::WPR + wc];
+            const uint32_t pfx = PF16[b * C::WPR + wc];
+            uint32_t cur = (!(st & 1u) && ((tm | um) & 1u)) ? lab_of(TBL[pfx - 1]) : kBG;
+            {
+                const uint16_t* e = TBL + pfx;
+                uint32_t tt = st;
+                while (tt) {
+                    const uint32_t bb = __ffs(tt) - 1;
+                    tt &= tt - 1;
+                    *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(*e++);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint4* p0 = reinterpret_cast<uint4*>(row0 + ((c ^ sw0) << 4));
+                uint4* p1 = reinterpret_cast<uint4*>(row1 + ((c ^ sw1) << 4));
+                const uint4 v = *p0;
+                uint32_t a[4] = {v.x, v.y, v.z, v.w}, a1[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = 4 * c + q;
+                    cur = ((st >> i) & 1u) ? a[q] : cur;
+                    a[q] = ((tm >> i) & 1u) ? cur : kBG;
+                    a1[q] = ((um >> i) & 1u) ? cur : kBG;
+                }
+                if (TMA_ST) {
+                    *p0 = make_uint4(a[0], a[1], a[2], a[3]);
+                    *p1 = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t gx = x0 + wc * 32 + 4 * c + q;
+                        if (gx < g.W && y0 + r0 < g.H) Lf[size_t(y0 + r0) * g.W + gx] = a[q];
+                        if (gx < g.W && y0 + r1 < g.H) Lf[size_t(y0 + r1) * g.W + gx] = a1[q];
+                    }
+                }
+            }
+            if (TMA_ST) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    for (int kk = 0; kk < 2; ++kk) {
+                        uint8_t* sk = smem + E::STG_OFF + (warp * 2 + kk) * 4096;
+                        tma_store_3d_hint(&tm_lab, int(x0 + wc * 32), int(y0 + 64 * wy + 32 * kk), int(ti.fz), sk,
+                                          policy_evict_first());
+                    }
+                }
+            }
+        } else {
 #pragma unroll 1
         for (int k = 0; k < C::WPL; ++k) {  // this lane's row words, one 32x32 staging tile each
             const int wc = wx * C::WPL + k;
             uint8_t* stg = smem + E::STG_OFF + (warp * C::WPL + k) * 4096;  // 32 x 32 u32, 128B-swizzled
             uint8_t* myrow = stg + lane * 128;
             const uint32_t m = M[row * C::WPR + wc];
-            const uint32_t lm = wc > 0 ? M[row * C::WPR + wc - 1] : 0u;
-            const uint32_t st = word_starts<RUNS>(m, lm);
-            const uint32_t pfx = PF16[row * C::WPR + wc];
-            uint32_t cur = ((st & 1u) || !(m & 1u)) ? kBG : lab_of(TBL[pfx - 1]);  // run continuing from the left
+            uint32_t st, pfx;
+            bool cont;  // the word starts inside a node continuing from the word on its left
+            if (BAND) {  // node starts are the band starts of rows (2b, 2b+1); prefixes per (band, word)
+                const int b = row >> 1;
+                st = BSt[b * C::WPR + wc];
+                pfx = PF16[b * C::WPR + wc];
+                const uint32_t partner = __shfl_xor_sync(0xffffffffu, m, 1);  // the other row of the band
+                cont = !(st & 1u) && ((m | partner) & 1u);
+            } else {
+                const uint32_t lm = wc > 0 ? M[row * C::WPR + wc - 1] : 0u;
+                st = word_starts<RUNS>(m, lm);
+                pfx = PF16[row * C::WPR + wc];
+                cont = !(st & 1u) && (m & 1u);
+            }
+            uint32_t cur = cont ? lab_of(TBL[pfx - 1]) : kBG;  // node continuing from the left
             {
                 const uint16_t* e = TBL + pfx;
                 uint32_t tt = st;
@@ -857,6 +1313,7 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
                         tma_store_3d(&tm_lab, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg);
                 }
             }
+        }
         }
         if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
@@ -940,7 +1397,30 @@ static cudaError_t launch_local_v(const LaunchArgs& a) {
     return cudaGetLastError();
 }
 
+static bool uses_band(const LaunchArgs& a) { return CCL_BAND && a.variant == 0; }
+
+static cudaError_t launch_local_band(const LaunchArgs& a) {
+    using C = BandCfg;
+    using A = ALayout<C, true, true>;
+    const uint32_t nt = tile_count(a);
+    cudaError_t e;
+    if (a.tma_load) {
+        auto k = k_local_band<C, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
+        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, 6)), C::NT, A::SMEM, a.stream, false, a.tm_img,
+                      a.img, a.work, a.g, nt);
+    } else {
+        auto k = k_local_band<C, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, 7)), C::NT, A::SMEM, a.stream, false, a.tm_img,
+                      a.img, a.work, a.g, nt);
+    }
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_local(const LaunchArgs& a) {
+    if (uses_band(a)) return launch_local_band(a);
     switch (a.variant) {
         case 0: return launch_local_v<0>(a);
         case 1: return launch_local_v<1>(a);
@@ -949,31 +1429,32 @@ cudaError_t launch_local(const LaunchArgs& a) {
     }
 }
 
-template <bool RUNS>
+template <bool RUNS, bool BAND>
 static cudaError_t launch_final_v(const LaunchArgs& a) {
-    using C = ECfg;
-    using E = ELayout<C, RUNS>;
+    using C = typename std::conditional<BAND, BandECfg, ECfg>::type;
+    using E = ELayout<C, RUNS, BAND>;
     const uint32_t nt = tile_count(a);
     cudaError_t e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
                                a.g, nt);
     if (e != cudaSuccess) return e;
     if (a.tma_store) {
-        auto k = k_final<C, RUNS, true>;
+        auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 0 : 1)), C::NT, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, BAND ? 2 : (RUNS ? 0 : 1))), C::NT, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
-        auto k = k_final<C, RUNS, false>;
+        auto k = k_final<C, RUNS, false, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, RUNS ? 2 : 3)), C::NT, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, BAND ? 3 : (RUNS ? 0 : 1))), C::NT, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_final(const LaunchArgs& a) {
-    return (a.variant == 0 || a.variant == 1) ? launch_final_v<true>(a) : launch_final_v<false>(a);
+    if (uses_band(a)) return launch_final_v<true, true>(a);
+    return (a.variant == 0 || a.variant == 1) ? launch_final_v<true, false>(a) : launch_final_v<false, false>(a);
 }
 
 cudaError_t launch_seams(const LaunchArgs& a) {

@@ -77,7 +77,7 @@ class StripLabeler:
                                            self.full_h, out.data_ptr(), self.work.data_ptr(), self.scratch.data_ptr(),
                                            s))
         _check(_lib.ccl_strip_final(c, self.w, self.h, self.row0, self.full_h, out.data_ptr(), self.work.data_ptr(),
-                                    s))
+                                    v, s))
         return out
 
 
@@ -109,5 +109,5 @@ def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx
         _check(_lib.ccl_strip_seam_resolve(ctx.handle, seams.data_ptr(), n_strips, k, w, h, r0, h_full, lo.data_ptr(),
                                            wk.data_ptr(), scratch.data_ptr(), s))
     for k, (im, lo, r0, h, wk) in enumerate(views):
-        _check(_lib.ccl_strip_final(ctx.handle, w, h, r0, h_full, lo.data_ptr(), wk.data_ptr(), s))
+        _check(_lib.ccl_strip_final(ctx.handle, w, h, r0, h_full, lo.data_ptr(), wk.data_ptr(), v, s))
     return out

@@ -174,3 +174,17 @@ def test_random_image_device_matches_host(ccl):
             r0 = h // 3
             strip = ccl.random_image_device(w, h - r0, d, s, row0=r0).cpu().numpy()
             assert np.array_equal(strip, full[r0:]), (w, h, d, s, r0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["c2fl", "rc2fl", "cc2fl", "nc2fl"])
+def test_virtual_strips_variants(ccl, oracle_mod, variant):
+    # every variant through the strip protocol (ccl_strip_final must expand the
+    # node layout the strip's kernel (a) used), aligned and unaligned pitches
+    import torch
+    from paper_1712_09789_b200.strips import label_strips_single_gpu
+    th = ccl.tile_shape()[1]
+    for (w, h, n) in [(256, 4 * th, 3), (97, 3 * th + 5, 2)]:
+        img = ccl.random_image(w, h, 0.55, 11 + w)
+        got = label_strips_single_gpu(torch.from_numpy(img).cuda(), n, variant=variant).cpu().numpy()
+        assert np.array_equal(got, oracle_mod.sequential_ccl(img)), (variant, w, h, n)
