@@ -690,6 +690,23 @@ __device__ __forceinline__ uint32_t band_starts(uint32_t t, uint32_t u, uint32_t
     const uint32_t cl = (((tl >> 31) & t) | ((ul >> 31) & u)) & 1u;  // bit 0 linked to the word on the left
     return (t | u) & ~((lk << 1) | cl);
 }
+// First set bit of x in every segment of a word, segments starting at the bits
+// of `starts` (a segmented prefix-OR by doubling: bit p may look back k bits
+// while no segment starts in (p-k, p]).
+__device__ __forceinline__ uint32_t seg_first(uint32_t x, uint32_t starts) {
+    const uint32_t can = ~starts;
+    uint32_t inc = x, c = can;
+    inc |= (inc << 1) & c;
+    c &= c << 1;
+    inc |= (inc << 2) & c;
+    c &= c << 2;
+    inc |= (inc << 4) & c;
+    c &= c << 4;
+    inc |= (inc << 8) & c;
+    c &= c << 8;
+    inc |= (inc << 16) & c;
+    return x & ~((inc << 1) & can);
+}
 template <class C>
 __device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, int w) {
     const uint32_t t = M[(2 * band) * C::WPR + w], u = M[(2 * band + 1) * C::WPR + w];
@@ -867,44 +884,56 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             const uint32_t o = tm[k] & ua[k];
             const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
             const uint32_t os = (o & ~(o << 1)) & ~ocont;
-            uint32_t firstm = 0u;
-            uint32_t tt = bs[k], id = pfx[k];
             const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
-            while (tt) {
-                const uint32_t a = __ffs(tt) - 1;
-                tt &= tt - 1;
-                const uint32_t nx = tt ? __ffs(tt) - 1 : 32u;
-                const uint32_t span = (0xFFFFFFFFu << a) & (nx < 32 ? ~(0xFFFFFFFFu << nx) : 0xFFFFFFFFu);
-                const uint32_t ov = o & span;
-                uint32_t v;
-                if (ov) {
-                    const uint32_t f = __ffs(ov) - 1;
-                    firstm |= 1u << f;
-                    v = node_of(upfx[k], ubs[k], f);
-                } else {
-                    const uint32_t tb = tm[k] & span;
-                    if (tb) {
-                        v = kRoot | (rowpos0 + __ffs(tb) - 1);
-                    } else {
-                        uint32_t pos = rowpos1 + a;  // no top-row pixel in this word's part
-                        if (nx == 32) {              // the run may continue: look for a later top-row pixel
-                            for (int w = wc + 1; w < WPR; ++w) {
-                                const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
-                                const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
-                                const uint32_t below = bw ? (1u << (__ffs(bw) - 1)) - 1u : 0xFFFFFFFFu;
-                                const uint32_t cont = (tw | uw) & below;  // the part continuing from the left
-                                const uint32_t tc = tw & cont;
-                                if (tc) {
-                                    pos = uint32_t(r0 * C::TW + 32 * w) + __ffs(tc) - 1;
-                                    break;
-                                }
-                                if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
-                            }
+            // the part of the word before its first band start belongs to a band
+            // run of the word on the left (that lane owns the node)
+            const uint32_t contp = bs[k] ? (1u << (__ffs(bs[k]) - 1)) - 1u : 0xFFFFFFFFu;
+            const uint32_t firstm = seg_first(o, bs[k]) & ~contp;   // first overlap of each band run
+            const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
+            {   // every band run starts as a root coded by its first bottom-row column ...
+                uint16_t* dst = P + pfx[k];
+                uint32_t tt = bs[k];
+                while (tt) {
+                    const uint32_t a = __ffs(tt) - 1;
+                    tt &= tt - 1;
+                    *dst++ = node_t(kRoot | (rowpos1 + a));
+                }
+            }
+            {   // ... or by its first top-row pixel (the minimum pixel when it has one) ...
+                uint32_t tt = tfirst;
+                while (tt) {
+                    const uint32_t f = __ffs(tt) - 1;
+                    tt &= tt - 1;
+                    P[node_of(pfx[k], bs[k], f)] = node_t(kRoot | (rowpos0 + f));
+                }
+            }
+            if (bs[k] && (((tm[k] | um[k]) >> 31) & 1u)) {
+                // ... the last band run reaches the word's end: with no top-row pixel
+                // and no overlap here, its top-row pixel may lie in a later word
+                const uint32_t a = 31u - __clz(bs[k]);
+                const uint32_t span = 0xFFFFFFFFu << a;
+                if (!((tfirst | firstm) & span)) {
+                    for (int w = wc + 1; w < WPR; ++w) {
+                        const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
+                        const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
+                        const uint32_t below = bw ? (1u << (__ffs(bw) - 1)) - 1u : 0xFFFFFFFFu;
+                        const uint32_t cont = (tw | uw) & below;  // the part continuing from the left
+                        const uint32_t tc = tw & cont;
+                        if (tc) {
+                            P[pfx[k] + __popc(bs[k]) - 1] = node_t(kRoot | (uint32_t(r0 * C::TW + 32 * w) + __ffs(tc) - 1));
+                            break;
                         }
-                        v = kRoot | pos;
+                        if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
                     }
                 }
-                P[id++] = node_t(v);
+            }
+            {   // ... unless it overlaps the band above: coarse link to the band run there
+                uint32_t ff = firstm;
+                while (ff) {
+                    const uint32_t f = __ffs(ff) - 1;
+                    ff &= ff - 1;
+                    P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
+                }
             }
             U[k] = os & ~firstm;  // remaining overlaps
         }
