@@ -707,6 +707,21 @@ __device__ __forceinline__ uint32_t seg_first(uint32_t x, uint32_t starts) {
     inc |= (inc << 16) & c;
     return x & ~((inc << 1) & can);
 }
+// Bits of every segment (as in seg_first) that hold a set bit of x at or after them.
+__device__ __forceinline__ uint32_t seg_back(uint32_t x, uint32_t starts) {
+    const uint32_t can = ~(starts >> 1);  // bit p may look at p + 1
+    uint32_t inc = x, c = can;
+    inc |= (inc >> 1) & c;
+    c &= c >> 1;
+    inc |= (inc >> 2) & c;
+    c &= c >> 2;
+    inc |= (inc >> 4) & c;
+    c &= c >> 4;
+    inc |= (inc >> 8) & c;
+    c &= c >> 8;
+    inc |= (inc >> 16) & c;
+    return inc;
+}
 template <class C>
 __device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, int w) {
     const uint32_t t = M[(2 * band) * C::WPR + w], u = M[(2 * band + 1) * C::WPR + w];
@@ -890,29 +905,37 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             const uint32_t contp = bs[k] ? (1u << (__ffs(bs[k]) - 1)) - 1u : 0xFFFFFFFFu;
             const uint32_t firstm = seg_first(o, bs[k]) & ~contp;   // first overlap of each band run
             const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
-            {   // every band run starts as a root coded by its first bottom-row column ...
-                uint16_t* dst = P + pfx[k];
-                uint32_t tt = bs[k];
+            {   // a band run without a top-row pixel: a root coded by its first column
+                uint32_t tt = bs[k] & ~seg_back(tfirst, bs[k]);
                 while (tt) {
                     const uint32_t a = __ffs(tt) - 1;
                     tt &= tt - 1;
-                    *dst++ = node_t(kRoot | (rowpos1 + a));
+                    P[node_of(pfx[k], bs[k], a)] = node_t(kRoot | (rowpos1 + a));
                 }
             }
-            {   // ... or by its first top-row pixel (the minimum pixel when it has one) ...
-                uint32_t tt = tfirst;
+            {   // with one: coarse link to the band run above holding its first
+                // overlap (o is inside tm: the run's first overlap, when it has one,
+                // precedes the next run's first top-row pixel), else a root coded by
+                // its first top-row pixel
+                uint32_t tt = tfirst, ff = firstm;
                 while (tt) {
                     const uint32_t f = __ffs(tt) - 1;
                     tt &= tt - 1;
-                    P[node_of(pfx[k], bs[k], f)] = node_t(kRoot | (rowpos0 + f));
+                    const uint32_t nxt = tt ? __ffs(tt) - 1 : 32u;
+                    const uint32_t gg = ff ? __ffs(ff) - 1 : 32u;
+                    uint32_t v = kRoot | (rowpos0 + f);
+                    if (gg < nxt) {
+                        v = node_of(upfx[k], ubs[k], gg);
+                        ff &= ff - 1;
+                    }
+                    P[node_of(pfx[k], bs[k], f)] = node_t(v);
                 }
             }
             if (bs[k] && (((tm[k] | um[k]) >> 31) & 1u)) {
-                // ... the last band run reaches the word's end: with no top-row pixel
-                // and no overlap here, its top-row pixel may lie in a later word
+                // the last band run reaches the word's end: with no top-row pixel
+                // here, its top-row pixel may lie in a later word
                 const uint32_t a = 31u - __clz(bs[k]);
-                const uint32_t span = 0xFFFFFFFFu << a;
-                if (!((tfirst | firstm) & span)) {
+                if (!(tfirst & (0xFFFFFFFFu << a))) {
                     for (int w = wc + 1; w < WPR; ++w) {
                         const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
                         const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
@@ -925,14 +948,6 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                         }
                         if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
                     }
-                }
-            }
-            {   // ... unless it overlaps the band above: coarse link to the band run there
-                uint32_t ff = firstm;
-                while (ff) {
-                    const uint32_t f = __ffs(ff) - 1;
-                    ff &= ff - 1;
-                    P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
                 }
             }
             U[k] = os & ~firstm;  // remaining overlaps
