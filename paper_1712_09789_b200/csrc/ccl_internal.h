@@ -28,6 +28,9 @@
 #ifndef CCL_EMINB
 #define CCL_EMINB 2
 #endif
+#ifndef CCL_BULCAP
+#define CCL_BULCAP 96  // band kernel union pairs per warp (sized for 10 resident CTAs per SM)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

@@ -96,14 +96,20 @@ struct ALayout {
     static constexpr int M_OFF = FB_OFF + ((MAXN / 32 * 4 + 127) / 128) * 128;  // row-word masks
     static constexpr int PF16_OFF = M_OFF + C::MW * 4;                     // u16 prefixes (contiguous: one bulk store)
     static constexpr int BS_OFF = PF16_OFF + C::MW * 2;                    // band starts (band kernel)
-    static constexpr int PF_OFF = BS_OFF + (BAND ? C::BSW * 4 : 0);        // u32 counts / prefixes
-    static constexpr int BT_OFF = PF_OFF + C::MW * 4;                      // band totals (+ total)
-    static constexpr int FR_OFF = BT_OFF + 128;                            // [count, global idx of seam roots]
-    static constexpr int UL_CAP = CCL_ULCAP;                               // union pairs per warp
+    static constexpr int PF_OFF = BS_OFF + (BAND ? C::BSW * 4 : 0);        // u32 counts / prefixes (row kernel)
+    static constexpr int BT_OFF = PF_OFF + (BAND ? 0 : C::MW * 4);         // band totals (+ total)
+    static constexpr int FR_OFF = BT_OFF + (BAND && C::WY == 1 ? 0 : 128);  // [count, global idx of seam roots]
+    static constexpr int UL_CAP = BAND ? CCL_BULCAP : CCL_ULCAP;           // union pairs per warp
     static constexpr int UL_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
     static constexpr int IMG_OFF = UL_OFF + C::NWARP * UL_CAP * 4;
     static constexpr int BAR_OFF = IMG_OFF + C::PX;
-    static constexpr int SMEM = BAR_OFF + 64 + 1024;  // +1024: runtime base alignment slack
+    // band kernel: the prefix counts live in the seam-root list (written only
+    // after the last prefix read and a barrier); its TMA load is unswizzled,
+    // so a 128 B base alignment is enough
+    static constexpr int CNT_OFF = BAND ? FR_OFF + 16 : PF_OFF;
+    static constexpr int ALIGN = BAND ? 128 : 1024;
+    static constexpr int SMEM = BAR_OFF + (BAND ? 16 : 64) + ALIGN;  // + runtime base alignment slack
+    static_assert(!BAND || (C::TH / 2) * C::WX * 4 + 16 <= C::MAXF * 4, "band counts fit in the seam-root list");
 };
 
 // Kernel (e) shared memory: 3 head/mask stages, 2 table/label stages, staging.
@@ -184,9 +190,10 @@ __device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b) {
 // offset is added to the __shared__ array itself (no integer round trip), so
 // the compiler keeps the shared address space: LDS/STS with 32-bit addresses
 // instead of generic 64-bit LD/ST.
+template <uint32_t ALIGN = 1024>
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t off = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    const uint32_t off = (ALIGN - (smem_u32(smem_raw) & (ALIGN - 1))) & (ALIGN - 1);
     return smem_raw + off;
 }
 
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     uint32_t* FB = reinterpret_cast<uint32_t*>(smem + A::FB_OFF);
     uint32_t* M = reinterpret_cast<uint32_t*>(smem + A::M_OFF);
     uint16_t* PF16 = reinterpret_cast<uint16_t*>(smem + A::PF16_OFF);
-    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::PF_OFF);
+    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::CNT_OFF);
     uint32_t* BT = reinterpret_cast<uint32_t*>(smem + A::BT_OFF);
     uint32_t* FR = reinterpret_cast<uint32_t*>(smem + A::FR_OFF);
     uint8_t* IMG = smem + A::IMG_OFF;
@@ -755,13 +762,13 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
     static_assert(C::RPL == 2, "lane = 2-row band");
     using A = ALayout<C, true, true>;
     constexpr int WPL = C::WPL, WPR = C::WPR;
-    uint8_t* smem = aligned_smem();
+    uint8_t* smem = aligned_smem<A::ALIGN>();
     node_t* P = reinterpret_cast<node_t*>(smem + A::P_OFF);
     uint32_t* FB = reinterpret_cast<uint32_t*>(smem + A::FB_OFF);
     uint32_t* M = reinterpret_cast<uint32_t*>(smem + A::M_OFF);
     uint16_t* PF16 = reinterpret_cast<uint16_t*>(smem + A::PF16_OFF);  // per (band, word)
     uint32_t* BS = reinterpret_cast<uint32_t*>(smem + A::BS_OFF);      // band starts per (band, word)
-    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::PF_OFF);
+    uint32_t* CNT = reinterpret_cast<uint32_t*>(smem + A::CNT_OFF);
     uint32_t* BT = reinterpret_cast<uint32_t*>(smem + A::BT_OFF);
     uint32_t* FR = reinterpret_cast<uint32_t*>(smem + A::FR_OFF);
     uint8_t* IMG = smem + A::IMG_OFF;
