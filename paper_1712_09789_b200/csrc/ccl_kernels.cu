@@ -101,7 +101,8 @@ struct ALayout {
     static constexpr int FR_OFF = BT_OFF + (BAND && C::WY == 1 ? 0 : 128);  // [count, global idx of seam roots]
     static constexpr int UL_CAP = BAND ? CCL_BULCAP : CCL_ULCAP;           // union pairs per warp
     static constexpr int UL_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
-    static constexpr int IMG_OFF = UL_OFF + C::NWARP * UL_CAP * 4;
+    static constexpr int BN_OFF = UL_OFF + C::NWARP * UL_CAP * 4;          // border-pixel nodes (band kernel)
+    static constexpr int IMG_OFF = BN_OFF + (BAND ? (C::MAXF * 2 + 127) / 128 * 128 : 0);
     static constexpr int BAR_OFF = IMG_OFF + C::PX;
     // band kernel: the prefix counts live in the seam-root list (written only
     // after the last prefix read and a barrier); its TMA load is unswizzled,
@@ -773,6 +774,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
     uint32_t* FR = reinterpret_cast<uint32_t*>(smem + A::FR_OFF);
     uint8_t* IMG = smem + A::IMG_OFF;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
+    uint16_t* BN = reinterpret_cast<uint16_t*>(smem + A::BN_OFF);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
@@ -791,11 +793,6 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         mbar_init(bar, 1);
         if (blockIdx.x < ntiles) issue_at(tile_of(blockIdx.x, g));
     }
-    // node of the pixel (r, c) of a tile (the pixel must be foreground)
-    auto node_px = [&](int r, int c) -> uint32_t {
-        const int w = c >> 5;
-        return node_of(PF16[(r >> 1) * WPR + w], BS[(r >> 1) * WPR + w], uint32_t(c & 31));
-    };
 
     uint32_t it = 0;
     TileWalk walk(blockIdx.x, gridDim.x, g);
@@ -864,6 +861,26 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             pfx[k] = k > 0 ? pfx[k - 1] + __popc(bs[k - 1]) : pfx0;
             PF16[band * WPR + wc0 + k] = uint16_t(pfx[k]);
             BS[band * WPR + wc0 + k] = bs[k];
+        }
+        {   // node of every border pixel, in seam-record order [top | bottom | left | right]
+            // (0xFFFF = background): top / bottom rows from bands 0 / last by shuffles
+            static_assert(WPL == 1 && C::WY == 1, "border nodes: one word per lane, one warp row");
+            const uint32_t t0 = __shfl_sync(0xffffffffu, tm[0], 0), s0 = __shfl_sync(0xffffffffu, bs[0], 0);
+            const uint32_t p0 = __shfl_sync(0xffffffffu, pfx[0], 0);
+            const uint32_t u1 = __shfl_sync(0xffffffffu, um[0], 31), s1 = __shfl_sync(0xffffffffu, bs[0], 31);
+            const uint32_t p1 = __shfl_sync(0xffffffffu, pfx[0], 31);
+            const int c = 32 * wc0 + lane;
+            BN[c] = ((t0 >> lane) & 1u) ? uint16_t(node_of(p0, s0, lane)) : uint16_t(0xFFFFu);
+            BN[C::TW + c] = ((u1 >> lane) & 1u) ? uint16_t(node_of(p1, s1, lane)) : uint16_t(0xFFFFu);
+            if (wc0 == 0) {  // column 0 starts a band run
+                BN[2 * C::TW + r0] = (tm[0] & 1u) ? uint16_t(pfx[0]) : uint16_t(0xFFFFu);
+                BN[2 * C::TW + r1] = (um[0] & 1u) ? uint16_t(pfx[0]) : uint16_t(0xFFFFu);
+            }
+            if (wc0 == WPR - 1) {  // column TW-1 is in the word's last band run
+                const uint16_t last = uint16_t(pfx[0] + __popc(bs[0]) - 1u);
+                BN[2 * C::TW + C::TH + r0] = (tm[0] >> 31) ? last : uint16_t(0xFFFFu);
+                BN[2 * C::TW + C::TH + r1] = (um[0] >> 31) ? last : uint16_t(0xFFFFu);
+            }
         }
         if (C::WY > 1) __syncthreads();  // lane 0 of a lower warp row reads the band above from smem
         // the band above (lane - 1, or the warp row above): bottom row, starts, prefixes
@@ -1019,14 +1036,10 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
-            int r, c;
-            bool act;
-            if (i < C::TW) { r = 0; c = i; act = has_top; }
-            else if (i < 2 * C::TW) { r = C::TH - 1; c = i - C::TW; act = has_bot; }
-            else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; act = has_left; }
-            else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; act = has_right; }
-            if (!act || !((M[r * WPR + (c >> 5)] >> (c & 31)) & 1u)) continue;
-            uint32_t x = node_px(r, c), p = P[x];
+            const bool act = i < C::TW ? has_top : i < 2 * C::TW ? has_bot : i < 2 * C::TW + C::TH ? has_left : has_right;
+            uint32_t x = BN[i];
+            if (!act || x == 0xFFFFu) continue;
+            uint32_t p = P[x];
             while (!(p & kRoot)) {
                 x = p;
                 p = P[x];
@@ -1071,23 +1084,19 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         }
 
         // ---- seam records + strip-edge rows
+        const bool edge_top = ty == 0 && g.edge_above, edge_bot = ty + 1 == g.nty && g.edge_below;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
-            int r, c;
-            if (i < C::TW) { r = 0; c = i; }
-            else if (i < 2 * C::TW) { r = C::TH - 1; c = i - C::TW; }
-            else if (i < 2 * C::TW + C::TH) { r = i - 2 * C::TW; c = 0; }
-            else { r = i - 2 * C::TW - C::TH; c = C::TW - 1; }
+            const uint32_t x = BN[i];
             uint32_t v = kBG;
-            if ((M[r * WPR + (c >> 5)] >> (c & 31)) & 1u) {
-                const uint32_t code = P[node_px(r, c)];
+            if (x != 0xFFFFu) {
+                const uint32_t code = P[x];
                 if (code & kSeam) v = FR[1 + (code & kCode)];
             }
             wt[C::W_REC + i] = v;
             if (i < 2 * C::TW) {
                 const bool top = i < C::TW;
-                const bool edge = top ? (ty == 0 && g.edge_above) : (ty + 1 == g.nty && g.edge_below);
-                const uint32_t gx = x0 + c;
-                if (edge && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
+                const uint32_t gx = x0 + (top ? i : i - C::TW);
+                if ((top ? edge_top : edge_bot) && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
             }
         }
     }
