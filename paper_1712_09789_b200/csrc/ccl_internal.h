@@ -31,6 +31,9 @@
 #ifndef CCL_BULCAP
 #define CCL_BULCAP 96  // band kernel union pairs per warp (sized for 10 resident CTAs per SM)
 #endif
+#ifndef CCL_ETBL
+#define CCL_ETBL 3072  // band kernel (e): node-table stage capacity (sized for 4 CTAs/SM)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

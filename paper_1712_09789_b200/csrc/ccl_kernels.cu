@@ -118,7 +118,10 @@ template <class C, bool RUNS, bool BAND = false>
 struct ELayout {
     static constexpr int S1B = BAND ? C::S1_BYTES_BAND : C::S1_BYTES;
     static constexpr int S1 = (S1B + 127) / 128 * 128;
-    static constexpr int TBLB = RUNS ? C::PX : 2 * C::PX;                 // u16 node table
+    // u16 node table; band tiles with more than TBLN nodes (checkerboard-like)
+    // read their table from the work tile in global memory instead
+    static constexpr int TBLN = BAND ? CCL_ETBL : (RUNS ? C::PX / 2 : C::PX);
+    static constexpr int TBLB = TBLN * 2;
     static constexpr int S2 = (C::MAXF * 4 + TBLB + 127) / 128 * 128;     // resolved labels + table
     static constexpr int S1_OFF = 0;
     static constexpr int S2_OFF = S1_OFF + 3 * S1;
@@ -1196,7 +1199,8 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), E::S1B, &b1[j]);
     };
     auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
-        const uint32_t lb = (head[0] * 4 + 15) & ~15u, tb = (head[1] * 2 + 15) & ~15u;
+        const uint32_t lb = (head[0] * 4 + 15) & ~15u;
+        const uint32_t tb = head[1] <= uint32_t(E::TBLN) ? (head[1] * 2 + 15) & ~15u : 0u;
         const uint32_t* wt = work_tile<C>(const_cast<uint32_t*>(work), t);
         mbar_expect_tx(&b2[j], lb + tb);
         if (lb) bulk_load(s2buf(j), wt + C::W_LIST, lb, &b2[j]);
@@ -1249,6 +1253,9 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         }
         uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;
         if constexpr (C::RPL == 2) {
+            // (a lambda called once per table location, so the shared-memory
+            // table keeps LDS and the global fallback uses LDG)
+            auto expand = [&](const uint16_t* tbl) {
             // lane = band (rows 2b, 2b+1) of word column wx: the band starts are
             // walked once and both rows are filled (two 32x32 staging tiles per warp)
             const int b = wy * 32 + lane, wc = wx;
@@ -1261,9 +1268,9 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
             const uint32_t tm = M[r0 * C::WPR + wc], um = M[r1 * C::WPR + wc];
             const uint32_t st = BSt[b * C::WPR + wc];
             const uint32_t pfx = PF16[b * C::WPR + wc];
-            uint32_t cur = (!(st & 1u) && ((tm | um) & 1u)) ? lab_of(TBL[pfx - 1]) : kBG;
+            uint32_t cur = (!(st & 1u) && ((tm | um) & 1u)) ? lab_of(tbl[pfx - 1]) : kBG;
             {
-                const uint16_t* e = TBL + pfx;
+                const uint16_t* e = tbl + pfx;
                 uint32_t tt = st;
                 while (tt) {
                     const uint32_t bb = __ffs(tt) - 1;
@@ -1307,6 +1314,9 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
                     }
                 }
             }
+            };
+            if (M[-4 + 1] <= uint32_t(E::TBLN)) expand(TBL);
+            else expand(reinterpret_cast<const uint16_t*>(work_tile<C>(const_cast<uint32_t*>(work), t) + C::W_TBL));
         } else {
 #pragma unroll 1
         for (int k = 0; k < C::WPL; ++k) {  // this lane's row words, one 32x32 staging tile each
