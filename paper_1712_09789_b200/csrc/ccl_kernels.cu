@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
     }
 
     uint32_t it = 0;
+    CCL_PH_INIT();
     TileWalk walk(blockIdx.x, gridDim.x, g);
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
         const TileId ti = walk.cur;
@@ -807,6 +808,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
+        CCL_PH(8);
         for (int i = tid; i < A::MAXN / 32; i += C::NT) FB[i] = 0u;
         if (tid == 0) FR[0] = 0u;
 
@@ -836,6 +838,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             }
         }
         __syncthreads();
+        CCL_PH(9);
         if (TMA && tid == 0 && t + gridDim.x < ntiles) {
             TileWalk nx = walk;
             nx.advance();
@@ -1007,6 +1010,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             }
         }
         __syncthreads();
+        CCL_PH(10);
 
         // ---- one pointer-jump round (no barrier after it: jumps and unions only
         // replace an entry by an ancestor, unions CAS root entries only)
@@ -1032,6 +1036,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             }
         }
         __syncthreads();
+        CCL_PH(11);
 
         // ---- seam-touching roots: every foreground pixel on a side facing a
         // neighbour tile / strip marks its root once (balanced over threads)
@@ -1058,6 +1063,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             }
         }
         __syncthreads();
+        CCL_PH(12);
 
         // ---- node table: every entry becomes its root's code
         {
@@ -1086,6 +1092,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
 
+        CCL_PH(13);
         // ---- seam records + strip-edge rows
         const bool edge_top = ty == 0 && g.edge_above, edge_bot = ty + 1 == g.nty && g.edge_below;
         for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
@@ -1102,8 +1109,10 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 if ((top ? edge_top : edge_bot) && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
             }
         }
+        CCL_PH(14);
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    CCL_PH_DONE();
     pdl_trigger();
 }
 

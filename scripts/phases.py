@@ -10,7 +10,9 @@ import torch  # noqa: E402
 
 import paper_1712_09789_b200 as ccl  # noqa: E402
 
-NAMES = ["records+top", "masks", "prefix+coarse", "jumps", "unions", "flatten+marks", "tagging", "table"]
+NAMES = ["records+top", "masks", "prefix+coarse", "jumps", "unions", "flatten+marks", "tagging", "table",
+         "B:wait prev", "B:mask wait+build", "B:bands+coarse+ulist", "B:jumps+unions", "B:marks", "B:table+store",
+         "B:records"]
 lib = ccl._lib
 f = lib.ccl_debug_phases
 f.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
@@ -36,4 +38,6 @@ for kind in kinds:
     tot = sum(vals) or 1
     print(f"{kind}: total {tot / 1e6:.1f} Mcycles (thread-0 sum over CTAs per run)")
     for i, nm in enumerate(NAMES):
+        if not vals[i]:
+            continue
         print(f"  {nm:16s} {vals[i] / 1e6:8.2f} M  {100 * vals[i] / tot:5.1f}%")
