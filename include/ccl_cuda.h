@@ -112,7 +112,9 @@ ccl_status ccl_strip_final(ccl_ctx* ctx, uint32_t w, uint32_t h, uint32_t row0, 
 /* d_scratch for ccl_strip_seam_resolve must hold ccl_strip_scratch_words(n_strips, w) u32;
  * d_work (kernel (a) -> kernel (e) hand-off: per-tile masks, run table and
  * seam-root list) must hold ccl_work_bytes(w, h, 1) bytes and stay untouched
- * between ccl_strip_local and ccl_strip_final of the same strip. */
+ * between ccl_strip_local and ccl_strip_final of the same strip.  Zero-fill it
+ * once after allocating it (it carries kernel (a)'s per-seam flags, which
+ * are tagged with a per-launch id, so it can be reused without clearing). */
 size_t ccl_strip_scratch_words(uint32_t n_strips, uint32_t w);
 size_t ccl_work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
 

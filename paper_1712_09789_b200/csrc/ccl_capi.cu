@@ -3,6 +3,7 @@
 // (pipeline.cpp:13-15, image.hpp:31-38), TMA descriptor setup, staging and
 // timing.  No exception crosses this boundary; every CUDA failure becomes a
 // status code plus a thread-local message.
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -79,6 +80,17 @@ struct ccl_ctx {
 
 namespace {
 
+// Launch ids for kernel (a)'s fused seam flags: unique in the process (work
+// buffers may be shared between contexts), never 0 (a zero-filled buffer).
+uint32_t next_epoch() {
+    static std::atomic<uint32_t> counter{0};
+    uint32_t e;
+    do {
+        e = ++counter;
+    } while (e == 0);
+    return e;
+}
+
 ccl_status check_dims(uint32_t w, uint32_t h) {
     if (w == 0 || h == 0) return fail(CCL_EINVAL, "image dimensions must be at least 1x1");
     if (uint64_t(w) * h > uint64_t(CCL_BACKGROUND) - 1) return fail(CCL_EINVAL, "image exceeds 2^32-2 pixels");
@@ -146,6 +158,7 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
 ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events, bool split = false) {
     ctx->last_split = events && split;
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[0], a.stream));
+    a.g.epoch = next_epoch();
     CCL_CHECK(cclk::launch_local(a));
     if (ctx->last_split) CCL_CHECK(cudaEventRecord(ctx->ev[1], a.stream));
     CCL_CHECK(cclk::launch_seams(a));
@@ -175,6 +188,7 @@ ccl_status ensure_work(ccl_ctx* ctx, size_t bytes) {
     ctx->d_work = nullptr;
     ctx->d_work_bytes = 0;
     CCL_CHECK(cudaMalloc(&ctx->d_work, bytes));
+    CCL_CHECK(cudaMemset(ctx->d_work, 0, bytes));  // seam flags start clear
     ctx->d_work_bytes = bytes;
     return CCL_OK;
 }
@@ -326,6 +340,7 @@ ccl_status ccl_strip_local(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
     a.work = static_cast<uint32_t*>(d_work);
+    a.g.epoch = next_epoch();
     CCL_CHECK(cclk::launch_local(a));
     CCL_CHECK(cclk::launch_seams(a));
     return CCL_OK;

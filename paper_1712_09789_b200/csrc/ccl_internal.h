@@ -34,6 +34,9 @@
 #ifndef CCL_ETBL
 #define CCL_ETBL 3072  // band kernel (e): node-table stage capacity (sized for 4 CTAs/SM)
 #endif
+#ifndef CCL_FUSE_SEAMS
+#define CCL_FUSE_SEAMS 0  // band kernel (a) unions each tile seam itself (second finisher); no kernel (d)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif
@@ -72,6 +75,7 @@ struct Geo {
     size_t img_pitch;       // bytes between image rows
     size_t frame_pitch;     // bytes between frames (batch)
     size_t frame_px;        // labels per frame (W*H)
+    uint32_t epoch;         // per-launch id (never 0): fused seam flags of kernel (a)
 };
 
 struct LaunchArgs {

@@ -759,6 +759,28 @@ __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b) {
     }
 }
 
+// Algorithm 2 on 32 pixel pairs of a seam (records ra / rb, chunk c): a pair
+// whose predecessor along the seam is also foreground on both sides joins the
+// same two local components and is skipped; one union per distinct (a, b)
+// pair of the warp.  Records are read at L2 (another CTA may have written them
+// in this launch).
+__device__ __forceinline__ void seam_chunk(const Forest& fst, const uint32_t* ra, const uint32_t* rb, uint32_t c,
+                                           int lane) {
+    const uint32_t i = c * 32 + lane;
+    const uint32_t a = __ldcg(ra + i), b = __ldcg(rb + i);
+    const bool fg = (a != kBG) && (b != kBG);
+    bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
+    if (lane == 0) prev = c > 0 && __ldcg(ra + i - 1) != kBG && __ldcg(rb + i - 1) != kBG;
+    bool act = fg && !prev;
+#if CCL_SEAM_MATCH
+    // the same two components often meet several times along 32 seam pixels
+    const uint64_t key = act ? (uint64_t(a) << 32 | b) : ~0ull;
+    const uint32_t same = __match_any_sync(0xffffffffu, key);
+    act = act && (__ffs(same) - 1 == lane);
+#endif
+    if (act) fst.unite(a, b);
+}
+
 template <class C, bool TMA>
 __global__ void __launch_bounds__(C::NT, CCL_BMINB)
     k_local_band(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img, uint32_t* work, Geo g,
@@ -1109,6 +1131,38 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 if ((top ? edge_top : edge_bot) && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
             }
         }
+#if CCL_FUSE_SEAMS
+        // ---- kernel (d) fused: with this tile's records and seam roots published,
+        // each internal seam is unioned by whichever of its two tiles finishes
+        // second (epoch exchange on the seam's flag; nobody waits)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();  // cumulative over the barrier: publishes the whole CTA's stores
+            const uint32_t ep = g.epoch;
+            uint32_t todo = 0;
+            if (ty > 0 && atomicExch(work_tile<C>(work, t - g.ntx) + C::W_HEAD + 2, ep) == ep) todo |= 1u;
+            if (ty + 1 < g.nty && atomicExch(wt + C::W_HEAD + 2, ep) == ep) todo |= 2u;
+            if (tx > 0 && atomicExch(work_tile<C>(work, t - 1) + C::W_HEAD + 3, ep) == ep) todo |= 4u;
+            if (tx + 1 < g.ntx && atomicExch(wt + C::W_HEAD + 3, ep) == ep) todo |= 8u;
+            if (todo) __threadfence();
+            FR[0] = todo;
+        }
+        __syncthreads();
+        if (const uint32_t todo = FR[0]) {
+            constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
+            for (uint32_t j = warp; j < 2 * HC + 2 * VC; j += C::NWARP) {
+                const uint32_t s = j < HC ? 0u : j < 2 * HC ? 1u : j < 2 * HC + VC ? 2u : 3u;
+                if (!((todo >> s) & 1u)) continue;
+                const uint32_t c = s < 2 ? j - s * HC : j - 2 * HC - (s - 2) * VC;
+                const uint32_t *ra, *rb;  // (upper, lower) or (left, right) records
+                if (s == 0) { ra = work_tile<C>(work, t - g.ntx) + C::W_REC + C::TW; rb = wt + C::W_REC; }
+                else if (s == 1) { ra = wt + C::W_REC + C::TW; rb = work_tile<C>(work, t + g.ntx) + C::W_REC; }
+                else if (s == 2) { ra = work_tile<C>(work, t - 1) + C::W_REC + 2 * C::TW + C::TH; rb = wt + C::W_REC + 2 * C::TW; }
+                else { ra = wt + C::W_REC + 2 * C::TW + C::TH; rb = work_tile<C>(work, t + 1) + C::W_REC + 2 * C::TW; }
+                seam_chunk(fst, ra, rb, c, lane);
+            }
+        }
+#endif
         CCL_PH(14);
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1151,20 +1205,7 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
     } else {
         return;  // whole warp
     }
-    const uint32_t i = c * 32 + lane;
-    const uint32_t a = ra[i], b = rb[i];
-    const bool fg = (a != kBG) && (b != kBG);
-    bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
-    if (lane == 0) prev = c > 0 && ra[i - 1] != kBG && rb[i - 1] != kBG;
-    bool act = fg && !prev;
-#if CCL_SEAM_MATCH
-    // one union per distinct (a, b) pair of local roots in the warp: the same
-    // two components often meet several times along 32 seam pixels
-    const uint64_t key = act ? (uint64_t(a) << 32 | b) : ~0ull;
-    const uint32_t same = __match_any_sync(0xffffffffu, key);
-    act = act && (__ffs(same) - 1 == lane);
-#endif
-    if (act) fst.unite(a, b);
+    seam_chunk(fst, ra, rb, c, lane);
 }
 
 // ------------------------------------------------------------------ kernel (d2)
@@ -1538,6 +1579,7 @@ cudaError_t launch_final(const LaunchArgs& a) {
 
 cudaError_t launch_seams(const LaunchArgs& a) {
     using C = TileCfg;
+    if (CCL_FUSE_SEAMS && uses_band(a)) return cudaSuccess;  // kernel (a) did the seams
     const uint64_t warps = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
     if (warps == 0) return cudaSuccess;
     const dim3 grid(unsigned((warps * 32 + 255) / 256), a.nframes);

@@ -57,7 +57,7 @@ class StripLabeler:
         self.rank, self.world, self.group = rank, world, group
         self.seam = torch.empty(4 * w, dtype=torch.int32, device=device)
         self.scratch = torch.empty(int(_lib.ccl_strip_scratch_words(world, w)), dtype=torch.int32, device=device)
-        self.work = torch.empty(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=device)
+        self.work = torch.zeros(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=device)
 
     def label(self, img, out, variant="c2fl", stream=None):
         import torch
@@ -99,7 +99,7 @@ def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx
     views = []
     for k, (r0, h) in enumerate(parts):
         im, lo = img[r0:r0 + h], out[r0:r0 + h]
-        wk = torch.empty(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=img.device)
+        wk = torch.zeros(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=img.device)
         views.append((im, lo, r0, h, wk))
         _check(_lib.ccl_strip_local(ctx.handle, im.data_ptr(), im.stride(0), w, h, r0, h_full, lo.data_ptr(),
                                     wk.data_ptr(), v, s))
