@@ -37,6 +37,9 @@
 #ifndef CCL_FUSE_SEAMS
 #define CCL_FUSE_SEAMS 0  // band kernel (a) unions each tile seam itself (second finisher); no kernel (d)
 #endif
+#ifndef CCL_SEAM_K
+#define CCL_SEAM_K 4  // kernel (d): 32-pair seam chunks per warp (unions compacted over the warp)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

@@ -1178,34 +1178,69 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 template <class C>
 __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t ntiles) {
     constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
+    constexpr int K = CCL_SEAM_K;                          // chunks per warp
+    __shared__ uint2 list[8][32 * K];                      // this warp's unions
     const uint32_t fz = blockIdx.y;
     const Forest fst = forest_of<C>(work, ntiles);
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     pdl_wait();
     pdl_trigger();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t nh = (g.nty - 1) * g.ntx * HC;
     const uint32_t nv = (g.ntx - 1) * g.nty * VC;
-    const uint32_t *ra, *rb;
-    uint32_t c;
-    if (gw < nh) {  // horizontal seam: bottom record of (tx, ty) vs top record of (tx, ty + 1)
-        const uint32_t s = gw / HC;
-        c = gw - s * HC;
-        const uint32_t ty = s / g.ntx, tx = s - ty * g.ntx;
-        const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
-        ra = work + ta * C::TILE_WORDS + C::W_REC + C::TW;
-        rb = work + (ta + g.ntx) * C::TILE_WORDS + C::W_REC;
-    } else if (gw < nh + nv) {  // vertical seam: right record of (tx, ty) vs left record of (tx + 1, ty)
-        const uint32_t u = gw - nh, s = u / VC;
-        c = u - s * VC;
-        const uint32_t ty = s / (g.ntx - 1), tx = s - ty * (g.ntx - 1);
-        const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
-        ra = work + ta * C::TILE_WORDS + C::W_REC + 2 * C::TW + C::TH;
-        rb = work + (ta + 1) * C::TILE_WORDS + C::W_REC + 2 * C::TW;
-    } else {
-        return;  // whole warp
+    // records of K consecutive chunks, all loads in flight together
+    uint32_t va[K], vb[K], c[K];
+    bool prev0[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t gc = gw * K + k;
+        const uint32_t *ra = nullptr, *rb = nullptr;
+        c[k] = 0;
+        if (gc < nh) {  // horizontal seam: bottom record of (tx, ty) vs top record of (tx, ty + 1)
+            const uint32_t s = gc / HC;
+            c[k] = gc - s * HC;
+            const uint32_t ty = s / g.ntx, tx = s - ty * g.ntx;
+            const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
+            ra = work + ta * C::TILE_WORDS + C::W_REC + C::TW;
+            rb = work + (ta + g.ntx) * C::TILE_WORDS + C::W_REC;
+        } else if (gc < nh + nv) {  // vertical seam: right record of (tx, ty) vs left record of (tx + 1, ty)
+            const uint32_t u = gc - nh, s = u / VC;
+            c[k] = u - s * VC;
+            const uint32_t ty = s / (g.ntx - 1), tx = s - ty * (g.ntx - 1);
+            const size_t ta = (size_t(fz) * g.nty + ty) * g.ntx + tx;
+            ra = work + ta * C::TILE_WORDS + C::W_REC + 2 * C::TW + C::TH;
+            rb = work + (ta + 1) * C::TILE_WORDS + C::W_REC + 2 * C::TW;
+        }
+        const uint32_t i = c[k] * 32 + lane;
+        va[k] = ra ? ra[i] : kBG;
+        vb[k] = ra ? rb[i] : kBG;
+        prev0[k] = lane == 0 && ra && c[k] > 0 && ra[i - 1] != kBG && rb[i - 1] != kBG;
     }
-    seam_chunk(fst, ra, rb, c, lane);
+    // Algorithm 2 per pair; a pair whose predecessor along the seam is also
+    // foreground on both sides joins the same two local components and is
+    // skipped; one union per distinct (a, b) pair of a chunk; the unions are
+    // compacted so that every lane of the warp climbs
+    uint32_t n = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const bool fg = (va[k] != kBG) && (vb[k] != kBG);
+        bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
+        if (lane == 0) prev = prev0[k];
+        bool act = fg && !prev;
+#if CCL_SEAM_MATCH
+        const uint64_t key = act ? (uint64_t(va[k]) << 32 | vb[k]) : ~0ull;
+        const uint32_t same = __match_any_sync(0xffffffffu, key);
+        act = act && (__ffs(same) - 1 == lane);
+#endif
+        const uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (act) list[wib][n + __popc(bal & ((1u << lane) - 1u))] = make_uint2(va[k], vb[k]);
+        n += __popc(bal);
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < n; j += 32) {
+        const uint2 pr = list[wib][j];
+        fst.unite(pr.x, pr.y);
+    }
 }
 
 // ------------------------------------------------------------------ kernel (d2)
@@ -1580,8 +1615,9 @@ cudaError_t launch_final(const LaunchArgs& a) {
 cudaError_t launch_seams(const LaunchArgs& a) {
     using C = TileCfg;
     if (CCL_FUSE_SEAMS && uses_band(a)) return cudaSuccess;  // kernel (a) did the seams
-    const uint64_t warps = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
-    if (warps == 0) return cudaSuccess;
+    const uint64_t chunks = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
+    if (chunks == 0) return cudaSuccess;
+    const uint64_t warps = (chunks + CCL_SEAM_K - 1) / CCL_SEAM_K;
     const dim3 grid(unsigned((warps * 32 + 255) / 256), a.nframes);
     const cudaError_t e = launch_pdl(k_seams<C>, grid, 256, 0, a.stream, a.work, a.g, tile_count(a));
     if (e != cudaSuccess) return e;
