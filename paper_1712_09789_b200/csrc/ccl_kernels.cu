@@ -1363,11 +1363,14 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
                     *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(*e++);
                 }
             }
+            uint4 vv[8];  // all read-backs first: the stores below may not be hoisted over
+#pragma unroll
+            for (int c = 0; c < 8; ++c) vv[c] = *reinterpret_cast<const uint4*>(row0 + ((c ^ sw0) << 4));
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint4* p0 = reinterpret_cast<uint4*>(row0 + ((c ^ sw0) << 4));
                 uint4* p1 = reinterpret_cast<uint4*>(row1 + ((c ^ sw1) << 4));
-                const uint4 v = *p0;
+                const uint4 v = vv[c];
                 uint32_t a[4] = {v.x, v.y, v.z, v.w}, a1[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
