@@ -1036,13 +1036,15 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 
         // ---- one pointer-jump round (no barrier after it: jumps and unions only
         // replace an entry by an ancestor, unions CAS root entries only)
-        {
+#pragma unroll 1
+        for (int j = 0; j < CCL_BJUMP; ++j) {
             volatile node_t* vP = P;
             for (uint32_t id = tid; id < nodes; id += C::NT) {
                 const uint32_t p = vP[id];
                 const uint32_t pp = (p & kRoot) ? p : vP[p];
                 if (!(pp & kRoot)) vP[id] = node_t(pp);
             }
+            if (j + 1 < CCL_BJUMP) __syncthreads();
         }
         // ---- refinement unions on root codes
         for (uint32_t k = lane; k < nul; k += 32) {
