@@ -153,6 +153,21 @@ void ccl_tile_shape(uint32_t* tile_w, uint32_t* tile_h);
 /* Number of kernel launches one ccl_label_device call makes. */
 int ccl_launches_per_label(void);
 
+/* Instrumented metrics mode (reference BlockMetrics and
+ * RunReport, forest.hpp:12-29, pipeline.hpp:15-26, pipeline.cpp:72-91): a
+ * separate build of this library with -DCCL_METRICS=1
+ * (libccl_b200_metrics1.so) counts, per 128x64 tile of kernel (a), the
+ * parent-link steps taken while finding roots and the CAS attempts of unions,
+ * plus the border-merge (kernel (d)) and resolve (kernel (d2)) totals.
+ * ccl_metrics_build() is 1 in that build; ccl_read_metrics() copies the
+ * counters of the last labeling call on ctx (single image or batch; strips are
+ * not instrumented): tile_find / tile_cas get tiles_x*tiles_y*n_frames u32 in
+ * row-major tile order (either may be null), phase4 = {border find steps,
+ * border CAS attempts, resolve find steps, 0}.  CCL_EINVAL in the product build. */
+int ccl_metrics_build(void);
+ccl_status ccl_read_metrics(ccl_ctx* ctx, uint32_t* tile_find, uint32_t* tile_cas, size_t n_tiles, uint64_t* phase4,
+                            uint32_t* tiles_x, uint32_t* tiles_y, uint32_t* n_frames);
+
 /* Host-side synthetic inputs, byte-identical to the reference generators
  * (generate.cpp:9-106).  kind: 0 stripes, 1 spiral, 2 blobs, 3 checkerboard. */
 ccl_status ccl_gen_random(uint8_t* out, uint32_t w, uint32_t h, double density, uint64_t seed);

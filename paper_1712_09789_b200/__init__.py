@@ -89,6 +89,8 @@ _sig("ccl_compact_device", _c, _vp, _vp, _u32, _u32, _vp, _vp, ctypes.POINTER(ct
 _sig("ccl_compact_scratch_words", _sz, _u32, _u32)
 _sig("ccl_tile_shape", None, _u32p, _u32p)
 _sig("ccl_launches_per_label", _c)
+_sig("ccl_metrics_build", _c)
+_sig("ccl_read_metrics", _c, _vp, _u32p, _u32p, _sz, ctypes.POINTER(ctypes.c_uint64), _u32p, _u32p, _u32p)
 _sig("ccl_gen_random", _c, _u8p, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
 _sig("ccl_gen_pattern", _c, _u8p, _c, _u32, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
 _sig("ccl_last_error", ctypes.c_char_p)
@@ -99,7 +101,7 @@ C_ABI_SYMBOLS = [
     "ccl_gen_random_device", "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
-    "ccl_launches_per_label", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
+    "ccl_launches_per_label", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
 ]
 
 _EINVAL, _ENOMEM, _ECUDA, _ENODEV = 1, 2, 3, 4
@@ -266,9 +268,64 @@ def label_image(img, cfg: BlockConfig | None = None, variant="c2fl", workers: in
     _check(_lib.ccl_label_host(_ctx(device).handle, a.ctypes.data_as(_u8p), w, h, out.ctypes.data_as(_u32p), int(v),
                                ctypes.byref(ms)))
     bx, by = -(-w // cfg.block_w), -(-h // cfg.block_h)
-    return RunReport(label_map=LabelMap(w, h, out), blocks_x=bx, blocks_y=by, wall_time_ms=float(ms.value),
-                     variant=v, cfg=cfg, worker_count=workers,
-                     per_block=[BlockMetrics(block_id=i) for i in range(bx * by)] if bx * by <= 1 << 16 else [])
+    rep = RunReport(label_map=LabelMap(w, h, out), blocks_x=bx, blocks_y=by, wall_time_ms=float(ms.value),
+                    variant=v, cfg=cfg, worker_count=workers,
+                    per_block=[BlockMetrics(block_id=i) for i in range(bx * by)] if bx * by <= 1 << 16 else [])
+    if metrics_build():  # instrumented library: counters per GPU tile (see read_metrics)
+        m = read_metrics(_ctx(device))
+        rep.blocks_x, rep.blocks_y = m["tiles_x"], m["tiles_y"]
+        rep.per_block = [BlockMetrics(i, int(f), int(c))
+                         for i, (f, c) in enumerate(zip(m["find"].ravel(), m["cas"].ravel()))]
+        rep.border_phase = BlockMetrics(0, m["border_find"], m["border_cas"])
+        rep.resolve_phase = BlockMetrics(0, m["resolve_find"], 0)
+    return rep
+
+
+def metrics_build() -> bool:
+    """True when the loaded library is the instrumented build (CCL_METRICS=1)."""
+    return bool(_lib.ccl_metrics_build())
+
+
+def read_metrics(ctx: "Context | None" = None, device: int = 0) -> dict:
+    """Counters of the last labeling call on ``ctx`` (instrumented build only;
+    reference BlockMetrics, forest.hpp:12-29): per 128x64 tile of kernel (a)
+    the parent-link steps of root finding and the CAS attempts of unions
+    (arrays shaped (frames, tiles_y, tiles_x)), plus the border-merge and
+    resolve totals."""
+    c = (ctx or _ctx(device)).handle
+    tx, ty, nf = _u32(), _u32(), _u32()
+    _check(_lib.ccl_read_metrics(c, None, None, 0, None, ctypes.byref(tx), ctypes.byref(ty), ctypes.byref(nf)))
+    n = tx.value * ty.value * nf.value
+    f = np.zeros(n, np.uint32)
+    a = np.zeros(n, np.uint32)
+    ph = (ctypes.c_uint64 * 4)()
+    _check(_lib.ccl_read_metrics(c, f.ctypes.data_as(_u32p), a.ctypes.data_as(_u32p), n, ph, ctypes.byref(tx),
+                                 ctypes.byref(ty), ctypes.byref(nf)))
+    shape = (nf.value, ty.value, tx.value)
+    return {"tiles_x": tx.value, "tiles_y": ty.value, "frames": nf.value, "find": f.reshape(shape),
+            "cas": a.reshape(shape), "border_find": int(ph[0]), "border_cas": int(ph[1]), "resolve_find": int(ph[2])}
+
+
+@dataclass
+class MetricsSummary:
+    """pipeline.hpp MetricsSummary: per-block grids and means."""
+    grid_w: int = 0
+    grid_h: int = 0
+    iterations_grid: list = field(default_factory=list)
+    atomics_grid: list = field(default_factory=list)
+    mean_iterations: float = 0.0
+    mean_atomics: float = 0.0
+
+
+def aggregate_metrics(report: RunReport) -> MetricsSummary:
+    """pipeline.cpp:72-91: grids of the per-block counters and their means."""
+    s = MetricsSummary(report.blocks_x, report.blocks_y)
+    s.iterations_grid = [m.findroot_iterations for m in report.per_block]
+    s.atomics_grid = [m.atomic_ops for m in report.per_block]
+    if report.per_block:
+        s.mean_iterations = sum(s.iterations_grid) / len(report.per_block)
+        s.mean_atomics = sum(s.atomics_grid) / len(report.per_block)
+    return s
 
 
 def compact_labels(lm: LabelMap) -> LabelMap:

@@ -4,6 +4,7 @@
 // timing.  No exception crosses this boundary; every CUDA failure becomes a
 // status code plus a thread-local message.
 #include <atomic>
+#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -74,6 +75,9 @@ struct ccl_ctx {
     uint8_t* h_ring = nullptr;  // pinned double buffer for chunked device->file copies
     cudaEvent_t ring_ev[2] = {nullptr, nullptr};
     size_t d_work_bytes = 0;
+    uint32_t* d_metrics = nullptr;  // instrumented builds: counters of the last call (Geo::metrics)
+    size_t d_metrics_bytes = 0;
+    uint32_t m_tx = 0, m_ty = 0, m_frames = 0;
     ccl_timing last{};
     bool last_split = false;
 };
@@ -157,6 +161,23 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
 // programmatic-dependent-launch chaining, so only timed calls pay for them).
 ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events, bool split = false) {
     ctx->last_split = events && split;
+#if CCL_METRICS
+    {   // instrumented build: zeroed counters for this call
+        const size_t bytes = 32 + size_t(a.g.ntx) * a.g.nty * a.nframes * 8;
+        if (ctx->d_metrics_bytes < bytes) {
+            if (ctx->d_metrics) cudaFree(ctx->d_metrics);
+            ctx->d_metrics = nullptr;
+            ctx->d_metrics_bytes = 0;
+            CCL_CHECK(cudaMalloc(&ctx->d_metrics, bytes));
+            ctx->d_metrics_bytes = bytes;
+        }
+        CCL_CHECK(cudaMemsetAsync(ctx->d_metrics, 0, bytes, a.stream));
+        a.g.metrics = ctx->d_metrics;
+        ctx->m_tx = a.g.ntx;
+        ctx->m_ty = a.g.nty;
+        ctx->m_frames = a.nframes;
+    }
+#endif
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[0], a.stream));
     a.g.epoch = next_epoch();
     CCL_CHECK(cclk::launch_local(a));
@@ -243,6 +264,7 @@ void ccl_ctx_destroy(ccl_ctx* c) {
     if (c->h_img) cudaFreeHost(c->h_img);
     if (c->h_lab) cudaFreeHost(c->h_lab);
     if (c->d_work) cudaFree(c->d_work);
+    if (c->d_metrics) cudaFree(c->d_metrics);
     if (c->d_aux) cudaFree(c->d_aux);
     if (c->h_ring) cudaFreeHost(c->h_ring);
     for (auto& e : c->ring_ev)
@@ -550,6 +572,31 @@ void ccl_tile_shape(uint32_t* tw, uint32_t* th) {
 }
 
 int ccl_launches_per_label(void) { return 4; }  // (a), (d), (d2) resolve, (e)
+
+int ccl_metrics_build(void) { return CCL_METRICS; }
+
+ccl_status ccl_read_metrics(ccl_ctx* ctx, uint32_t* tile_find, uint32_t* tile_cas, size_t n_tiles, uint64_t* phase4,
+                            uint32_t* tiles_x, uint32_t* tiles_y, uint32_t* n_frames) {
+    if (!ctx) return fail(CCL_EINVAL, "null context");
+    if (!CCL_METRICS) return fail(CCL_EINVAL, "not an instrumented build (compile with CCL_METRICS=1)");
+    if (!ctx->d_metrics) return fail(CCL_EINVAL, "no labeling call on this context yet");
+    if (tiles_x) *tiles_x = ctx->m_tx;
+    if (tiles_y) *tiles_y = ctx->m_ty;
+    if (n_frames) *n_frames = ctx->m_frames;
+    const size_t nt = size_t(ctx->m_tx) * ctx->m_ty * ctx->m_frames;
+    if ((tile_find || tile_cas) && n_tiles < nt) return fail(CCL_EINVAL, "tile buffers smaller than the tile grid");
+    DeviceGuard dg(ctx->device);
+    std::vector<uint32_t> h(8 + 2 * nt);
+    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
+    CCL_CHECK(cudaDeviceSynchronize());
+    CCL_CHECK(cudaMemcpy(h.data(), ctx->d_metrics, h.size() * 4, cudaMemcpyDeviceToHost));
+    if (phase4) std::memcpy(phase4, h.data(), 32);
+    for (size_t t = 0; t < nt; ++t) {
+        if (tile_find) tile_find[t] = h[8 + 2 * t];
+        if (tile_cas) tile_cas[t] = h[8 + 2 * t + 1];
+    }
+    return CCL_OK;
+}
 
 const char* ccl_last_error(void) { return g_err.c_str(); }
 

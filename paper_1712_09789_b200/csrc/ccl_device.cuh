@@ -16,9 +16,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef CCL_METRICS
+#define CCL_METRICS 0
+#endif
+
 namespace cclk {
 
 constexpr uint32_t kBG = 0xFFFFFFFFu;
+
+// Per-thread cost counters of an instrumented build (-DCCL_METRICS=1, a
+// separate library): the two cost drivers the reference reports per block
+// (BlockMetrics, forest.hpp:12-29) -- parent-link steps taken while finding
+// roots, and CAS attempts (successful or failed) of unions.  Empty otherwise.
+struct Ctr {
+#if CCL_METRICS
+    uint32_t f = 0, c = 0;
+    __device__ __forceinline__ void step(uint32_t n = 1) { f += n; }
+    __device__ __forceinline__ void cas() { ++c; }
+#else
+    __device__ __forceinline__ void step(uint32_t = 1) {}
+    __device__ __forceinline__ void cas() {}
+#endif
+};
 
 // ---------------------------------------------------------------- bit helpers
 // Foreground bits of 4 bytes: bit k set iff byte k == 1 (exact for any byte value).
@@ -92,9 +111,10 @@ struct Forest {
     }
     __device__ __forceinline__ uint32_t key(uint32_t n) const { return node(n).y; }
     // Root of x and the root's {parent, key}.
-    __device__ __forceinline__ uint32_t find(uint32_t x, uint2& v) const {
+    __device__ __forceinline__ uint32_t find(uint32_t x, uint2& v, Ctr& m) const {
         v = node(x);
         while (v.x != x) {
+            m.step();
             x = v.x;
             v = node(x);
         }
@@ -102,19 +122,20 @@ struct Forest {
     }
     __device__ __forceinline__ uint32_t find(uint32_t x) const {
         uint2 v;
-        return find(x, v);
+        Ctr m;
+        return find(x, v, m);
     }
     // find + path compression of x itself (later walks through x take one hop)
-    __device__ __forceinline__ uint2 find_compress(uint32_t x) const {
+    __device__ __forceinline__ uint2 find_compress(uint32_t x, Ctr& m) const {
         uint2 v;
-        const uint32_t r = find(x, v);
+        const uint32_t r = find(x, v, m);
         if (r != x) f[2 * size_t(x)] = r;
         return v;
     }
     // Min-key union: the root with the larger key is linked below the other
     // one with a CAS on its parent; both sides climb in lockstep so their
     // loads overlap (the common case is one load per side, then the CAS).
-    __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
+    __device__ __forceinline__ void unite(uint32_t a, uint32_t b, Ctr& m) const {
         uint2 A = node(a), B = node(b);
         for (;;) {
             bool ca = A.x != a, cb = B.x != b;
@@ -124,6 +145,7 @@ struct Forest {
                 if (cb) Bn = node(B.x);
                 // (no path halving here: at high density every union climbs
                 // through the same few hot nodes and the extra stores thrash)
+                m.step(uint32_t(ca) + uint32_t(cb));
                 if (ca) { a = A.x; A = An; ca = A.x != a; }
                 if (cb) { b = B.x; B = Bn; cb = B.x != b; }
             }
@@ -132,6 +154,7 @@ struct Forest {
                 const uint32_t t = a; a = b; b = t;
                 const uint2 T = A; A = B; B = T;
             }
+            m.cas();
             const uint32_t old = atomicCAS(f + 2 * size_t(a), a, b);
             if (old == a) return;
             a = old;  // a was linked meanwhile: continue from its new parent

@@ -43,6 +43,9 @@
 #ifndef CCL_BJUMP
 #define CCL_BJUMP 1  // band kernel (a): pointer-jumping rounds before the unions
 #endif
+#ifndef CCL_METRICS
+#define CCL_METRICS 0  // instrumented build: per-tile find / CAS counters (separate library)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif
@@ -82,6 +85,10 @@ struct Geo {
     size_t frame_pitch;     // bytes between frames (batch)
     size_t frame_px;        // labels per frame (W*H)
     uint32_t epoch;         // per-launch id (never 0): fused seam flags of kernel (a)
+    // instrumented builds (CCL_METRICS=1) only, else null: u64[4] phase totals
+    // {border find steps, border CAS attempts, resolve find steps, 0}, then
+    // u32[2] {find steps, CAS attempts} per tile of kernel (a)
+    uint32_t* metrics;
 };
 
 struct LaunchArgs {

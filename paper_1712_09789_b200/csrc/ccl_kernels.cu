@@ -164,10 +164,11 @@ __device__ unsigned long long g_phase_cycles[16];
 
 // Node parents are u16; unions are CAS min-unions on the 16-bit entries.
 using node_t = uint16_t;
-__device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
+__device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x, Ctr& m) {
     volatile node_t* vP = P;
     uint32_t p = vP[x];
     while (!(p & kRoot)) {
+        m.step();
         const uint32_t gp = vP[p];
         if (gp & kRoot) return p;
         vP[x] = node_t(gp);  // path halving (ancestor only)
@@ -176,18 +177,43 @@ __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x) {
     }
     return x;
 }
-__device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b) {
+__device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b, Ctr& m) {
     volatile node_t* vP = P;
     for (;;) {
-        a = nfind(P, a);
-        b = nfind(P, b);
+        a = nfind(P, a, m);
+        b = nfind(P, b, m);
         if (a == b) return;
         if (a < b) { const uint32_t t = a; a = b; b = t; }
         const uint32_t ca = vP[a];  // a's root code: link a below b unless a got linked meanwhile
+        if (ca & kRoot) m.cas();
         if ((ca & kRoot) && atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(ca),
                                       static_cast<unsigned short>(b)) == ca)
             return;
     }
+}
+
+// Instrumented builds: counters of a warp flushed to the per-tile grid / the
+// per-phase totals (layout in ccl_internal.h, Geo::metrics).  Whole warps only.
+__device__ __forceinline__ void metrics_tile(const Geo& g, uint32_t t, Ctr& m) {
+#if CCL_METRICS
+    const uint32_t f = __reduce_add_sync(0xffffffffu, m.f), c = __reduce_add_sync(0xffffffffu, m.c);
+    if ((threadIdx.x & 31) == 0 && g.metrics) {
+        if (f) atomicAdd(g.metrics + 8 + 2 * size_t(t), f);
+        if (c) atomicAdd(g.metrics + 8 + 2 * size_t(t) + 1, c);
+    }
+    m.f = m.c = 0;
+#endif
+}
+__device__ __forceinline__ void metrics_phase(const Geo& g, int k, Ctr& m) {
+#if CCL_METRICS
+    const uint32_t f = __reduce_add_sync(0xffffffffu, m.f), c = __reduce_add_sync(0xffffffffu, m.c);
+    if ((threadIdx.x & 31) == 0 && g.metrics) {
+        unsigned long long* ph = reinterpret_cast<unsigned long long*>(g.metrics);
+        if (f) atomicAdd(ph + k, static_cast<unsigned long long>(f));
+        if (c) atomicAdd(ph + k + 1, static_cast<unsigned long long>(c));
+    }
+    m.f = m.c = 0;
+#endif
 }
 
 // Dynamic shared memory rounded up to 1024 B (128B-swizzled TMA tiles).  The
@@ -373,6 +399,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
     }
 
     CCL_PH_INIT();
+    Ctr mc;  // instrumented builds: this thread's find steps / CAS attempts of the current tile
     uint32_t it = 0;
     TileWalk walk(blockIdx.x, gridDim.x, g);
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
@@ -534,6 +561,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 for (uint32_t id = tid; id < nodes; id += C::NT) {
                     const uint32_t p = vP[id];
                     const uint32_t pp = (p & kRoot) ? p : vP[p];
+                    if (!(p & kRoot)) mc.step();
                     if (!(pp & kRoot)) vP[id] = node_t(pp);
                 }
                 // no barrier after the last round: jumps and unions only ever
@@ -547,7 +575,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         {
             for (uint32_t k = lane; k < nul; k += 32) {
                 const uint32_t pr = UL[k];
-                nunion(P, pr & 0xFFFFu, pr >> 16);
+                nunion(P, pr & 0xFFFFu, pr >> 16, mc);
             }
 #pragma unroll
             for (int k = 0; k < C::WPL; ++k) {
@@ -555,7 +583,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 while (Uk) {                                          // pairs that did not fit in the list
                     const uint32_t b = __ffs(Uk) - 1;
                     Uk &= Uk - 1;
-                    nunion(P, node_of(pfx[k], st[k], b), node_of(upfx[k], ust[k], b));
+                    nunion(P, node_of(pfx[k], st[k], b), node_of(upfx[k], ust[k], b), mc);
                 }
                 if (!RUNS) {  // horizontal pixel pairs (incl. the word boundary), minus closed 2x2 squares
                     const uint32_t hm = m[k] & ((m[k] << 1) | ((lm[k] >> 31) & 1u));
@@ -565,7 +593,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                         const uint32_t b = __ffs(hp) - 1;
                         hp &= hp - 1;
                         const uint32_t id = node_of(pfx[k], st[k], b);
-                        nunion(P, id, id - 1);  // the left neighbour is the previous fg pixel in raster order
+                        nunion(P, id, id - 1, mc);  // the left neighbour is the previous fg pixel in raster order
                     }
                 }
             }
@@ -606,6 +634,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 }
                 uint32_t x = id, p = P[id];
                 while (!(p & kRoot)) {
+                    mc.step();
                     x = p;
                     p = P[x];
                 }
@@ -632,6 +661,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 uint32_t p = vP[id];
                 if (!(p & kRoot)) {
                     do {
+                        mc.step();
                         p = vP[p];
                     } while (!(p & kRoot));
                     vP[id] = node_t(p);
@@ -679,6 +709,7 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
                 if (edge && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
             }
         }
+        metrics_tile(g, t, mc);
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     CCL_PH_DONE();
@@ -741,11 +772,11 @@ __device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, 
 }
 // Min-union on root codes (positions): the root whose code is larger is
 // linked below the other with a CAS on its entry.
-__device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b) {
+__device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b, Ctr& m) {
     volatile node_t* vP = P;
     for (;;) {
-        a = nfind(P, a);
-        b = nfind(P, b);
+        a = nfind(P, a, m);
+        b = nfind(P, b, m);
         if (a == b) return;
         uint32_t ca = vP[a], cb = vP[b];
         if (!(ca & kRoot) || !(cb & kRoot)) continue;  // linked meanwhile: find again
@@ -753,6 +784,7 @@ __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b) {
             const uint32_t t = a; a = b; b = t;
             const uint32_t tc = ca; ca = cb; cb = tc;
         }
+        m.cas();
         if (atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(ca),
                       static_cast<unsigned short>(b)) == ca)
             return;
@@ -765,7 +797,7 @@ __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b) {
 // pair of the warp.  Records are read at L2 (another CTA may have written them
 // in this launch).
 __device__ __forceinline__ void seam_chunk(const Forest& fst, const uint32_t* ra, const uint32_t* rb, uint32_t c,
-                                           int lane) {
+                                           int lane, Ctr& mc) {
     const uint32_t i = c * 32 + lane;
     const uint32_t a = __ldcg(ra + i), b = __ldcg(rb + i);
     const bool fg = (a != kBG) && (b != kBG);
@@ -778,7 +810,7 @@ __device__ __forceinline__ void seam_chunk(const Forest& fst, const uint32_t* ra
     const uint32_t same = __match_any_sync(0xffffffffu, key);
     act = act && (__ffs(same) - 1 == lane);
 #endif
-    if (act) fst.unite(a, b);
+    if (act) fst.unite(a, b, mc);
 }
 
 template <class C, bool TMA>
@@ -821,6 +853,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 
     uint32_t it = 0;
     CCL_PH_INIT();
+    Ctr mc;  // instrumented builds: this thread's find steps / CAS attempts of the current tile
     TileWalk walk(blockIdx.x, gridDim.x, g);
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
         const TileId ti = walk.cur;
@@ -1042,6 +1075,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             for (uint32_t id = tid; id < nodes; id += C::NT) {
                 const uint32_t p = vP[id];
                 const uint32_t pp = (p & kRoot) ? p : vP[p];
+                if (!(p & kRoot)) mc.step();
                 if (!(pp & kRoot)) vP[id] = node_t(pp);
             }
             if (j + 1 < CCL_BJUMP) __syncthreads();
@@ -1049,14 +1083,14 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         // ---- refinement unions on root codes
         for (uint32_t k = lane; k < nul; k += 32) {
             const uint32_t pr = UL[k];
-            nunion_pos(P, pr & 0xFFFFu, pr >> 16);
+            nunion_pos(P, pr & 0xFFFFu, pr >> 16, mc);
         }
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             while (U[k]) {  // pairs that did not fit in the list
                 const uint32_t b = __ffs(U[k]) - 1;
                 U[k] &= U[k] - 1;
-                nunion_pos(P, node_of(pfx[k], bs[k], b), node_of(upfx[k], ubs[k], b));
+                nunion_pos(P, node_of(pfx[k], bs[k], b), node_of(upfx[k], ubs[k], b), mc);
             }
         }
         __syncthreads();
@@ -1073,6 +1107,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             if (!act || x == 0xFFFFu) continue;
             uint32_t p = P[x];
             while (!(p & kRoot)) {
+                mc.step();
                 x = p;
                 p = P[x];
             }
@@ -1096,6 +1131,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 uint32_t p = vP[id];
                 if (!(p & kRoot)) {
                     do {
+                        mc.step();
                         p = vP[p];
                     } while (!(p & kRoot));
                     vP[id] = node_t(p);
@@ -1161,10 +1197,11 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 else if (s == 1) { ra = wt + C::W_REC + C::TW; rb = work_tile<C>(work, t + g.ntx) + C::W_REC; }
                 else if (s == 2) { ra = work_tile<C>(work, t - 1) + C::W_REC + 2 * C::TW + C::TH; rb = wt + C::W_REC + 2 * C::TW; }
                 else { ra = wt + C::W_REC + 2 * C::TW + C::TH; rb = work_tile<C>(work, t + 1) + C::W_REC + 2 * C::TW; }
-                seam_chunk(fst, ra, rb, c, lane);
+                seam_chunk(fst, ra, rb, c, lane, mc);
             }
         }
 #endif
+        metrics_tile(g, t, mc);
         CCL_PH(14);
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1188,6 +1225,7 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
     pdl_wait();
     pdl_trigger();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    Ctr mc;
     const uint32_t nh = (g.nty - 1) * g.ntx * HC;
     const uint32_t nv = (g.ntx - 1) * g.nty * VC;
     // records of K consecutive chunks, all loads in flight together
@@ -1241,8 +1279,9 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
     __syncwarp();
     for (uint32_t j = lane; j < n; j += 32) {
         const uint2 pr = list[wib][j];
-        fst.unite(pr.x, pr.y);
+        fst.unite(pr.x, pr.y, mc);
     }
+    metrics_phase(g, 0, mc);
 }
 
 // ------------------------------------------------------------------ kernel (d2)
@@ -1259,7 +1298,9 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
     const Forest fst = forest_of<C>(work, ntiles);
-    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.find_compress(t * uint32_t(C::MAXF) + k).y;
+    Ctr mc;
+    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.find_compress(t * uint32_t(C::MAXF) + k, mc).y;
+    metrics_phase(g, 2, mc);
 }
 
 // ------------------------------------------------------------------ kernel (e)

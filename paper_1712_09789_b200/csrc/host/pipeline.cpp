@@ -73,6 +73,26 @@ RunReport label_image(const BinaryImage& img, const BlockConfig& cfg, Variant va
     check(ccl_label_host(thread_ctx(), img.data.data(), img.width, img.height, rep.label_map.labels.data(),
                          int(variant), &ms));
     rep.wall_time = std::chrono::duration<double, std::milli>(double(ms));
+    if (ccl_metrics_build()) {
+        // instrumented build: the counters are per GPU tile (the GPU's block),
+        // so per_block / blocks_x / blocks_y describe the tile grid
+        std::uint32_t tx = 0, ty = 0, nfr = 0;
+        std::uint64_t ph[4] = {0, 0, 0, 0};
+        check(ccl_read_metrics(thread_ctx(), nullptr, nullptr, 0, nullptr, &tx, &ty, &nfr));
+        std::vector<std::uint32_t> f(std::size_t(tx) * ty), c(f.size());
+        check(ccl_read_metrics(thread_ctx(), f.data(), c.data(), f.size(), ph, &tx, &ty, &nfr));
+        rep.blocks_x = tx;
+        rep.blocks_y = ty;
+        rep.per_block.assign(f.size(), BlockMetrics{});
+        for (std::size_t i = 0; i < f.size(); ++i) {
+            rep.per_block[i].block_id = std::uint32_t(i);
+            rep.per_block[i].findroot_iterations = f[i];
+            rep.per_block[i].atomic_ops = c[i];
+        }
+        rep.border_phase.findroot_iterations = ph[0];
+        rep.border_phase.atomic_ops = ph[1];
+        rep.resolve_phase.findroot_iterations = ph[2];
+    }
     return rep;
 }
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # bench.py (device value only) for every experiment library in _lib/
 cd "$(dirname "$0")/.."
-for lib in paper_1712_09789_b200/_lib/libccl_b200*.so; do
+for lib in $(ls paper_1712_09789_b200/_lib/libccl_b200*.so | grep -v metrics1); do
   echo "== $lib"; CCL_LIB_PATH=$lib timeout 300 python bench.py --no-cpu-baseline --steps 30 2>&1 | python -c "
 import json,sys
 try:

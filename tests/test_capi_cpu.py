@@ -107,3 +107,30 @@ def test_strip_split(ccl):
 def test_tile_shape(ccl):
     tw, th = ccl.tile_shape()
     assert tw % 32 == 0 and th % 32 == 0 and th <= 256
+
+
+def test_metrics_build_exports_and_product_refuses(ccl):
+    """The instrumented library (CCL_METRICS=1) exports the same C-ABI; the
+    product library reports it is not instrumented (no GPU calls)."""
+    path = os.path.join(os.path.dirname(ccl.lib_path()), "libccl_b200_metrics1.so")
+    assert os.path.exists(path), "build() also builds the metrics library"
+    inst = ctypes.CDLL(path)
+    prod = ctypes.CDLL(ccl.lib_path())
+    assert [s for s in _declared_c_functions() if not hasattr(inst, s)] == []
+    assert inst.ccl_metrics_build() == 1 and prod.ccl_metrics_build() == 0
+    assert not ccl.metrics_build()
+    f = prod.ccl_read_metrics
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_size_t] + [ctypes.c_void_p] * 4
+    assert f(None, None, None, 0, None, None, None, None) == 1  # CCL_EINVAL
+
+
+def test_aggregate_metrics_mirror(ccl):
+    """pipeline.cpp:72-91 restated: grids in block order and their means."""
+    lm = ccl.LabelMap(4, 4, np.zeros((4, 4), np.uint32))
+    rep = ccl.RunReport(lm, 2, 1, 0.0, ccl.Variant.C2FL, ccl.BlockConfig(), 1,
+                        per_block=[ccl.BlockMetrics(0, 3, 1), ccl.BlockMetrics(1, 5, 0)])
+    s = ccl.aggregate_metrics(rep)
+    assert (s.grid_w, s.grid_h) == (2, 1)
+    assert s.iterations_grid == [3, 5] and s.atomics_grid == [1, 0]
+    assert s.mean_iterations == 4.0 and s.mean_atomics == 0.5
