@@ -89,6 +89,12 @@ MetricsSummary aggregate_metrics(const RunReport& report);
 // labels are per-frame raster indices.
 std::vector<LabelMap> label_batch(const std::vector<BinaryImage>& frames, Variant variant = Variant::C2FL);
 
+// One image over several GPUs of this process (horizontal strips, seams
+// exchanged by peer copies; a device may repeat).  Same label map as
+// label_image; wall_time = max over strips of the device time.
+RunReport label_image_strips(const BinaryImage& img, const std::vector<int>& devices,
+                             Variant variant = Variant::C2FL);
+
 // CUDA device used by this host thread's implicit context (default 0).
 void set_device(int device);
 

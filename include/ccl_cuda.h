@@ -78,6 +78,16 @@ ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t
 ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pitch, size_t frame_pitch,
                            uint32_t n, uint32_t w, uint32_t h, uint32_t* d_labels, int variant, void* stream);
 
+/* One image over several devices in one process (the additive C++ entry point
+ * ccl::label_image_strips): devices[k] labels strip k (near-equal row bands,
+ * all but the last a multiple of the tile height) with the strip protocol
+ * below; seams are exchanged by peer copies.  A device may be listed more than
+ * once (virtual strips).  Host buffers; labels are global raster indices,
+ * bit-exact with ccl_label_host.  *kernel_ms = max over strips of the device
+ * time from the first kernel to the last (exchange included). */
+ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, uint32_t w, uint32_t h,
+                            uint32_t* labels, int variant, float* kernel_ms);
+
 /* ---- Strip mode (image split into horizontal strips, one per GPU/rank) ----
  * A strip holds rows [row0, row0+h) of a full image of `full_h` rows, width w;
  * every strip but the last must have h a multiple of the tile height

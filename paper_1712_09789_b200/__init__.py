@@ -90,6 +90,7 @@ _sig("ccl_compact_scratch_words", _sz, _u32, _u32)
 _sig("ccl_tile_shape", None, _u32p, _u32p)
 _sig("ccl_launches_per_label", _c)
 _sig("ccl_metrics_build", _c)
+_sig("ccl_label_strips", _c, ctypes.POINTER(_c), _c, _u8p, _u32, _u32, _u32p, _c, ctypes.POINTER(ctypes.c_float))
 _sig("ccl_read_metrics", _c, _vp, _u32p, _u32p, _sz, ctypes.POINTER(ctypes.c_uint64), _u32p, _u32p, _u32p)
 _sig("ccl_gen_random", _c, _u8p, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
 _sig("ccl_gen_pattern", _c, _u8p, _c, _u32, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
@@ -101,7 +102,7 @@ C_ABI_SYMBOLS = [
     "ccl_gen_random_device", "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
-    "ccl_launches_per_label", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
+    "ccl_launches_per_label", "ccl_label_strips", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
 ]
 
 _EINVAL, _ENOMEM, _ECUDA, _ENODEV = 1, 2, 3, 4
@@ -279,6 +280,26 @@ def label_image(img, cfg: BlockConfig | None = None, variant="c2fl", workers: in
         rep.border_phase = BlockMetrics(0, m["border_find"], m["border_cas"])
         rep.resolve_phase = BlockMetrics(0, m["resolve_find"], 0)
     return rep
+
+
+def label_strips(img, devices=(0,), variant="c2fl") -> RunReport:
+    """``ccl::label_image_strips``: one host image over the listed GPUs of this
+    process (horizontal strips, seams exchanged by peer copies; a device may
+    repeat), the same label map as ``label_image``."""
+    if len(devices) == 0:
+        raise ValueError("no devices")
+    v = Variant.parse(variant)
+    a = _as_image(img)
+    h, w = a.shape
+    out = np.empty((h, w), dtype=np.uint32)
+    ms = ctypes.c_float()
+    devs = (_c * len(devices))(*devices)
+    _check(_lib.ccl_label_strips(devs, len(devices), a.ctypes.data_as(_u8p), w, h, out.ctypes.data_as(_u32p), int(v),
+                                 ctypes.byref(ms)))
+    cfg = BlockConfig()
+    bx, by = -(-w // cfg.block_w), -(-h // cfg.block_h)
+    return RunReport(label_map=LabelMap(w, h, out), blocks_x=bx, blocks_y=by, wall_time_ms=float(ms.value),
+                     variant=v, cfg=cfg, worker_count=len(devices))
 
 
 def metrics_build() -> bool:

@@ -139,6 +139,25 @@ MetricsSummary aggregate_metrics(const RunReport& report) {
     return s;
 }
 
+RunReport label_image_strips(const BinaryImage& img, const std::vector<int>& devices, Variant variant) {
+    if (devices.empty()) throw std::invalid_argument("label_image_strips: no devices");
+    RunReport rep;
+    rep.variant = variant;
+    rep.worker_count = unsigned(devices.size());
+    rep.blocks_x = (img.width + rep.cfg.block_w - 1) / rep.cfg.block_w;
+    rep.blocks_y = (img.height + rep.cfg.block_h - 1) / rep.cfg.block_h;
+    rep.per_block.resize(std::size_t(rep.blocks_x) * rep.blocks_y);
+    for (std::size_t i = 0; i < rep.per_block.size(); ++i) rep.per_block[i].block_id = std::uint32_t(i);
+    rep.label_map = LabelMap(img.width, img.height);
+    if (img.data.size() != rep.label_map.labels.size())
+        throw std::invalid_argument("image data size does not match width*height");
+    float ms = 0.f;
+    check(ccl_label_strips(devices.data(), int(devices.size()), img.data.data(), img.width, img.height,
+                           rep.label_map.labels.data(), int(variant), &ms));
+    rep.wall_time = std::chrono::duration<double, std::milli>(double(ms));
+    return rep;
+}
+
 std::vector<LabelMap> label_batch(const std::vector<BinaryImage>& frames, Variant variant) {
     std::vector<LabelMap> out;
     if (frames.empty()) return out;

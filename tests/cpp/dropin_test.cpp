@@ -87,6 +87,23 @@ int main() {
         ref_label_image(frames[f].data.data(), 320, 200, 32, 32, 0, 1, w.data(), &ms);
         CHECK(maps[f].labels == w);
     }
+    // multi-device strips in one process (device 0 listed three times: virtual strips)
+    {
+        const ccl::BinaryImage im = ccl::random_image(1000, 700, 0.58, 77);
+        std::vector<std::uint32_t> w(im.pixel_count());
+        double ms;
+        ref_label_image(im.data.data(), 1000, 700, 32, 32, 0, 1, w.data(), &ms);
+        const ccl::RunReport r = ccl::label_image_strips(im, {0, 0, 0});
+        CHECK(r.label_map.labels == w);
+        CHECK(r.worker_count == 3);
+        bool threw = false;
+        try {
+            ccl::label_image_strips(im, {});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     std::printf(fails ? "dropin_test: %d failures\n" : "dropin_test: OK\n", fails);
     return fails ? 1 : 0;
 }

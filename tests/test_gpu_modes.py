@@ -188,3 +188,24 @@ def test_virtual_strips_variants(ccl, oracle_mod, variant):
         img = ccl.random_image(w, h, 0.55, 11 + w)
         got = label_strips_single_gpu(torch.from_numpy(img).cuda(), n, variant=variant).cpu().numpy()
         assert np.array_equal(got, oracle_mod.sequential_ccl(img)), (variant, w, h, n)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0]])
+@pytest.mark.parametrize("kind", ["random", "spiral", "checkerboard"])
+def test_label_strips_multi_device_api(ccl, oracle_mod, kind, devices):
+    """ccl_label_strips / label_strips: one host image over a device list (one
+    GPU listed n times = n strips with peer-copy seam exchange on one device)."""
+    w, h = 1003, 777
+    img = ccl.random_image(w, h, 0.58, 5) if kind == "random" else ccl.pattern_image(kind, w, h, period=5)
+    rep = ccl.label_strips(img, devices)
+    assert np.array_equal(rep.label_map.labels, oracle_mod.sequential_ccl(img)), (kind, devices)
+    assert rep.worker_count == len(devices) and rep.wall_time_ms > 0
+
+
+def test_label_strips_errors(ccl):
+    img = np.ones((100, 50), np.uint8)
+    with pytest.raises(ValueError):
+        ccl.label_strips(img, [])
+    th = ccl.tile_shape()[1]
+    with pytest.raises(ValueError):  # more strips than tile rows
+        ccl.label_strips(np.ones((th, 50), np.uint8), [0, 0])
