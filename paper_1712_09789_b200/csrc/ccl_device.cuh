@@ -19,6 +19,9 @@
 #ifndef CCL_METRICS
 #define CCL_METRICS 0
 #endif
+#ifndef CCL_UNITE_COMPRESS
+#define CCL_UNITE_COMPRESS 1  // kernel (d): both start nodes of a union point at the root afterwards
+#endif
 
 namespace cclk {
 
@@ -136,6 +139,17 @@ struct Forest {
     // one with a CAS on its parent; both sides climb in lockstep so their
     // loads overlap (the common case is one load per side, then the CAS).
     __device__ __forceinline__ void unite(uint32_t a, uint32_t b, Ctr& m) const {
+#if CCL_UNITE_COMPRESS
+        const uint32_t a0 = a, b0 = b;
+        // afterwards both start nodes point at the class root they reached: a
+        // tile's seam root meets many seams, and these are its own (cold) lines
+        auto done = [&](uint32_t r) {
+            if (a0 != r && a0 != a) f[2 * size_t(a0)] = r;
+            if (b0 != r && b0 != b) f[2 * size_t(b0)] = r;
+        };
+#else
+        auto done = [](uint32_t) {};
+#endif
         uint2 A = node(a), B = node(b);
         for (;;) {
             bool ca = A.x != a, cb = B.x != b;
@@ -149,14 +163,20 @@ struct Forest {
                 if (ca) { a = A.x; A = An; ca = A.x != a; }
                 if (cb) { b = B.x; B = Bn; cb = B.x != b; }
             }
-            if (a == b) return;
+            if (a == b) {
+                done(a);
+                return;
+            }
             if (A.y < B.y) {  // a: the root with the larger key
                 const uint32_t t = a; a = b; b = t;
                 const uint2 T = A; A = B; B = T;
             }
             m.cas();
             const uint32_t old = atomicCAS(f + 2 * size_t(a), a, b);
-            if (old == a) return;
+            if (old == a) {
+                done(b);
+                return;
+            }
             a = old;  // a was linked meanwhile: continue from its new parent
             A = node(a);
             B = node(b);
