@@ -1335,13 +1335,16 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         if (tb) bulk_load(s2buf(j) + C::MAXF, wt + C::W_TBL, tb, &b2[j]);
     };
     if (tid == 0 && TMA_ST) prefetch_tmap(&tm_lab);
-    pdl_wait();
     if (tid == 0) {
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
         for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
         const uint32_t t0 = blockIdx.x;
+        // heads / masks come from kernel (a), complete before (d2) let this grid
+        // launch; only the seam labels of (d2) need the dependency wait.  Every
+        // other thread reads global data only through thread 0's copies.
         if (t0 < ntiles) s1(t0, 0);
         if (t0 + G < ntiles) s1(t0 + G, 1);
+        pdl_wait();
         if (t0 < ntiles) {
             mbar_wait(&b1[0], 0);
             s2(t0, 0, s1buf(0));
