@@ -46,6 +46,12 @@
 #ifndef CCL_METRICS
 #define CCL_METRICS 0  // instrumented build: per-tile find / CAS counters (separate library)
 #endif
+#ifndef CCL_ABAL
+#define CCL_ABAL 0  // band kernel (a): persistent grid sized so every CTA walks the same number of tiles
+#endif
+#ifndef CCL_AIMG_OVERLAY
+#define CCL_AIMG_OVERLAY 1  // band kernel (a): TMA tile staged in the node table (no prefetch, -8 KB smem)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif
@@ -53,7 +59,7 @@
 #define CCL_BWPL 1  // 32-px row words per lane in the band kernel (a)
 #endif
 #ifndef CCL_BMINB
-#define CCL_BMINB 10  // min resident CTAs of the band kernel (a)
+#define CCL_BMINB 12  // min resident CTAs of the band kernel (a)
 #endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0

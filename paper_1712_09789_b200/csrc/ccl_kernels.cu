@@ -102,8 +102,13 @@ struct ALayout {
     static constexpr int UL_CAP = BAND ? CCL_BULCAP : CCL_ULCAP;           // union pairs per warp
     static constexpr int UL_OFF = ((FR_OFF + (1 + C::MAXF) * 4) + 127) / 128 * 128;
     static constexpr int BN_OFF = UL_OFF + C::NWARP * UL_CAP * 4;          // border-pixel nodes (band kernel)
-    static constexpr int IMG_OFF = BN_OFF + (BAND ? (C::MAXF * 2 + 127) / 128 * 128 : 0);
-    static constexpr int BAR_OFF = IMG_OFF + C::PX;
+    static constexpr int BN_END = BN_OFF + (BAND ? (C::MAXF * 2 + 127) / 128 * 128 : 0);
+    // band kernel with CCL_AIMG_OVERLAY: the TMA tile lands in the node table
+    // (dead between the table's bulk store and the next coarse scan)
+    static constexpr bool OVL = BAND && CCL_AIMG_OVERLAY;
+    static_assert(!OVL || MAXN * 2 >= C::PX, "tile bytes fit in the node table");
+    static constexpr int IMG_OFF = OVL ? P_OFF : BN_END;
+    static constexpr int BAR_OFF = OVL ? BN_END : IMG_OFF + C::PX;
     // band kernel: the prefix counts live in the seam-root list (written only
     // after the last prefix read and a barrier); its TMA load is unswizzled,
     // so a 128 B base alignment is enough
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         }
         __syncthreads();
         CCL_PH(9);
-        if (TMA && tid == 0 && t + gridDim.x < ntiles) {
+        if (TMA && !A::OVL && tid == 0 && t + gridDim.x < ntiles) {
             TileWalk nx = walk;
             nx.advance();
             issue_at(nx.cur);
@@ -1202,6 +1207,18 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         }
 #endif
         metrics_tile(g, t, mc);
+        if (TMA && A::OVL) {  // next tile into the node table once every reader is done with it
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (t + gridDim.x < ntiles) {
+                    TileWalk nx = walk;
+                    nx.advance();
+                    issue_at(nx.cur);
+                }
+            }
+        }
         CCL_PH(14);
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1559,6 +1576,14 @@ static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntil
 
 static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
 
+// Fewest CTAs that still finish in the same number of tile rounds: every CTA
+// then walks the same number of tiles (no half-empty last round).
+static unsigned balanced(unsigned grid, uint32_t ntiles) {
+    if (!CCL_ABAL || grid == 0 || ntiles <= grid) return grid;
+    const uint32_t rounds = (ntiles + grid - 1) / grid;
+    return unsigned((ntiles + rounds - 1) / rounds);
+}
+
 // Launch (optionally) with programmatic stream serialization: the kernel calls
 // pdl_wait() before reading what the previous kernel in the stream produced.
 template <class K, class... Args>
@@ -1612,8 +1637,8 @@ static cudaError_t launch_local_band(const LaunchArgs& a) {
         auto k = k_local_band<C, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, 6)), C::NT, A::SMEM, a.stream, false, a.tm_img,
-                      a.img, a.work, a.g, nt);
+        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt, 6), nt)), C::NT, A::SMEM, a.stream, false,
+                      a.tm_img, a.img, a.work, a.g, nt);
     } else {
         auto k = k_local_band<C, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
