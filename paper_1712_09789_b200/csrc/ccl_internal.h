@@ -58,6 +58,9 @@
 #ifndef CCL_EMINB2
 #define CCL_EMINB2 4  // min resident CTAs of the 8-warp band kernel (e) (caps registers at 64)
 #endif
+#ifndef CCL_ERESOLVE
+#define CCL_ERESOLVE 0  // band mode: kernel (d2) runs as a fifth warp of kernel (e)
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

@@ -1329,6 +1329,29 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
     metrics_phase(g, 2, mc);
 }
 
+// Kernel (d2) inside kernel (e) (CCL_ERESOLVE, band mode): the final label of
+// each of tile tt's nf seam roots into the shared-memory list FT, two finds per
+// lane climbing in lockstep (their L2 loads overlap).
+template <class C>
+__device__ __forceinline__ void resolve_tile(const Forest& fst, uint32_t tt, uint32_t nf, uint32_t* FT, int lane) {
+    const uint32_t base = tt * uint32_t(C::MAXF);
+    for (uint32_t k = lane; k < nf; k += 64) {
+        const bool two = k + 32 < nf;
+        uint32_t a = base + k, b = two ? a + 32 : a;
+        uint2 A = fst.node(a), B = fst.node(b);
+        bool ca = A.x != a, cb = B.x != b;
+        while (ca || cb) {
+            uint2 An = A, Bn = B;
+            if (ca) An = fst.node(A.x);
+            if (cb) Bn = fst.node(B.x);
+            if (ca) { a = A.x; A = An; ca = A.x != a; }
+            if (cb) { b = B.x; B = Bn; cb = B.x != b; }
+        }
+        FT[k] = A.y;
+        if (two) FT[k + 32] = B.y;
+    }
+}
+
 // ------------------------------------------------------------------ kernel (e)
 // Persistent, 3-stage pipeline per CTA: while tile i is expanded, the node
 // table + resolved seam labels of tile i+1 and the head/masks of tile i+2 are
@@ -1336,7 +1359,7 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
 // swizzled staging tile and writes it with one TMA store: every label is
 // written exactly once and the image is never re-read.
 template <class C, bool RUNS, bool TMA_ST, bool BAND>
-__global__ void __launch_bounds__(C::NT, C::HALF ? CCL_EMINB2 : CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+__global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::HALF ? CCL_EMINB2 : CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
                                                     const uint32_t* work, Geo g, uint32_t ntiles) {
     using E = ELayout<C, RUNS, BAND>;
     uint8_t* smem = aligned_smem();
@@ -1352,8 +1375,11 @@ __global__ void __launch_bounds__(C::NT, C::HALF ? CCL_EMINB2 : CCL_EMINB) k_fin
         mbar_expect_tx(&b1[j], E::S1B);
         bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), E::S1B, &b1[j]);
     };
+    // band mode with CCL_ERESOLVE: warp NWARP resolves the seam labels of the
+    // next tile into its stage (no kernel (d2)); the copies bring the table only
+    constexpr bool RES = BAND && CCL_ERESOLVE;
     auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
-        const uint32_t lb = (head[0] * 4 + 15) & ~15u;
+        const uint32_t lb = RES ? 0u : (head[0] * 4 + 15) & ~15u;
         const uint32_t tb = head[1] <= uint32_t(E::TBLN) ? (head[1] * 2 + 15) & ~15u : 0u;
         const uint32_t* wt = work_tile<C>(const_cast<uint32_t*>(work), t);
         mbar_expect_tx(&b2[j], lb + tb);
@@ -1363,7 +1389,7 @@ __global__ void __launch_bounds__(C::NT, C::HALF ? CCL_EMINB2 : CCL_EMINB) k_fin
     if (tid == 0 && TMA_ST) prefetch_tmap(&tm_lab);
     if (tid == 0) {
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
-        for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
+        for (int j = 0; j < 2; ++j) mbar_init(&b2[j], RES ? 2 : 1);
         const uint32_t t0 = blockIdx.x;
         // heads / masks come from kernel (a), complete before (d2) let this grid
         // launch; only the seam labels of (d2) need the dependency wait.  Every
@@ -1377,11 +1403,32 @@ __global__ void __launch_bounds__(C::NT, C::HALF ? CCL_EMINB2 : CCL_EMINB) k_fin
         }
     }
     __syncthreads();
+    const Forest fres = forest_of<C>(const_cast<uint32_t*>(work), ntiles);
+    if (RES && warp == C::NWARP) {  // the first tile's seam labels
+        pdl_wait();                 // the forest is final once the previous kernels are done
+        if (blockIdx.x < ntiles) {
+            mbar_wait(&b1[0], 0);
+            resolve_tile<C>(fres, blockIdx.x, s1buf(0)[0], s2buf(0), lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&b2[0]);
+        }
+    }
 
     const int sw = lane & 7;
     uint32_t it = 0;
     TileWalk walk(blockIdx.x, G, g);
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it, walk.advance()) {
+        if (RES && warp == C::NWARP) {  // resolver warp: the next tile's seam labels
+            if (t + G < ntiles) {
+                const uint32_t jn = (it + 1) % 3, jr = (it + 1) & 1u;
+                mbar_wait(&b1[jn], ((it + 1) / 3) & 1u);
+                resolve_tile<C>(fres, t + G, s1buf(jn)[0], s2buf(jr), lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&b2[jr]);
+            }
+            __syncthreads();  // pairs with the workers' end-of-tile barrier
+            continue;
+        }
         const uint32_t j1 = it % 3, j2 = it & 1u;
         if (tid == 0) {
             if (t + 2 * G < ntiles) s1(t + 2 * G, (it + 2) % 3);
@@ -1739,19 +1786,24 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
     using C = typename std::conditional<BAND, BE, ECfg>::type;
     using E = ELayout<C, RUNS, BAND>;
     const uint32_t nt = tile_count(a);
-    cudaError_t e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
-                               a.g, nt);
-    if (e != cudaSuccess) return e;
+    constexpr bool RES = BAND && CCL_ERESOLVE;  // (d2) runs inside (e)
+    constexpr int NTH = C::NT + (RES ? 32 : 0);
+    cudaError_t e = cudaSuccess;
+    if (!RES) {
+        e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
+                       a.g, nt);
+        if (e != cudaSuccess) return e;
+    }
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, BAND ? 2 : (RUNS ? 0 : 1))), C::NT, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid_x(k, NTH, E::SMEM, nt, BAND ? 2 : (RUNS ? 0 : 1))), NTH, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
         auto k = k_final<C, RUNS, false, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, C::NT, E::SMEM, nt, BAND ? 3 : (RUNS ? 0 : 1))), C::NT, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid_x(k, NTH, E::SMEM, nt, BAND ? 3 : (RUNS ? 0 : 1))), NTH, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     }
     return e != cudaSuccess ? e : cudaGetLastError();
