@@ -61,6 +61,9 @@
 #ifndef CCL_ERESOLVE
 #define CCL_ERESOLVE 0  // band mode: kernel (d2) runs as a fifth warp of kernel (e)
 #endif
+#ifndef CCL_ERES_Q
+#define CCL_ERES_Q 4  // CCL_ERESOLVE: finds per lane of the resolver warp in lockstep
+#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

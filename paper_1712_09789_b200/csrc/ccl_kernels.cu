@@ -1334,21 +1334,37 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
 // lane climbing in lockstep (their L2 loads overlap).
 template <class C>
 __device__ __forceinline__ void resolve_tile(const Forest& fst, uint32_t tt, uint32_t nf, uint32_t* FT, int lane) {
+    constexpr int Q = CCL_ERES_Q;  // finds per lane in lockstep
     const uint32_t base = tt * uint32_t(C::MAXF);
-    for (uint32_t k = lane; k < nf; k += 64) {
-        const bool two = k + 32 < nf;
-        uint32_t a = base + k, b = two ? a + 32 : a;
-        uint2 A = fst.node(a), B = fst.node(b);
-        bool ca = A.x != a, cb = B.x != b;
-        while (ca || cb) {
-            uint2 An = A, Bn = B;
-            if (ca) An = fst.node(A.x);
-            if (cb) Bn = fst.node(B.x);
-            if (ca) { a = A.x; A = An; ca = A.x != a; }
-            if (cb) { b = B.x; B = Bn; cb = B.x != b; }
+    for (uint32_t k0 = lane; k0 < nf; k0 += 32 * Q) {
+        uint32_t x[Q];
+        uint2 v[Q];
+        bool c[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint32_t k = k0 + 32u * q;
+            x[q] = base + (k < nf ? k : k0);
+            v[q] = fst.node(x[q]);
         }
-        FT[k] = A.y;
-        if (two) FT[k + 32] = B.y;
+        bool any = true;
+        while (any) {
+            any = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) c[q] = v[q].x != x[q];
+            uint2 n[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) n[q] = c[q] ? fst.node(v[q].x) : v[q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (c[q]) {
+                    x[q] = v[q].x;
+                    v[q] = n[q];
+                    any |= v[q].x != x[q];
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (k0 + 32u * q < nf) FT[k0 + 32u * q] = v[q].y;
     }
 }
 
