@@ -4,6 +4,7 @@
 // timing.  No exception crosses this boundary; every CUDA failure becomes a
 // status code plus a thread-local message.
 #include <atomic>
+#include <cstdlib>
 #include <algorithm>
 #include <thread>
 #include <vector>
@@ -77,6 +78,17 @@ struct ccl_ctx {
     uint8_t* h_ring = nullptr;  // pinned double buffer for chunked device->file copies
     cudaEvent_t ring_ev[2] = {nullptr, nullptr};
     size_t d_work_bytes = 0;
+    // CUDA graphs of the device path, keyed by the call's buffers and shape
+    struct Graph {
+        const void* img;
+        size_t pitch;
+        uint32_t w, h;
+        const void* lab;
+        int variant;
+        const void* work;
+        cudaGraphExec_t exec;
+    };
+    std::vector<Graph> graphs;
     uint32_t* d_metrics = nullptr;  // instrumented builds: counters of the last call (Geo::metrics)
     size_t d_metrics_bytes = 0;
     uint32_t m_tx = 0, m_ty = 0, m_frames = 0;
@@ -159,6 +171,26 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
     return CCL_OK;
 }
 
+// CUDA graphs for repeated device-path calls (off with CCL_GRAPHS=0; never in
+// instrumented or fused-seam builds: per-call memsets / launch epochs).
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("CCL_GRAPHS");
+        return !(v && v[0] == '0') && !CCL_METRICS && !CCL_FUSE_SEAMS;
+    }();
+    return on;
+}
+
+// One replay, bracketed by the context's events (the total time of the call,
+// as run_pipeline records it for direct launches).
+ccl_status launch_graph(ccl_ctx* ctx, cudaGraphExec_t exec, cudaStream_t st) {
+    ctx->last_split = false;
+    CCL_CHECK(cudaEventRecord(ctx->ev[0], st));
+    CCL_CHECK(cudaGraphLaunch(exec, st));
+    CCL_CHECK(cudaEventRecord(ctx->ev[3], st));
+    return CCL_OK;
+}
+
 // `split`: also time each kernel group (events between the launches break the
 // programmatic-dependent-launch chaining, so only timed calls pay for them).
 ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events, bool split = false) {
@@ -207,6 +239,8 @@ ccl_status read_timing(ccl_ctx* ctx, ccl_timing* t) {
 
 ccl_status ensure_work(ccl_ctx* ctx, size_t bytes) {
     if (ctx->d_work_bytes >= bytes) return CCL_OK;
+    for (auto& gr : ctx->graphs) cudaGraphExecDestroy(gr.exec);  // they point at the old buffer
+    ctx->graphs.clear();
     if (ctx->d_work) cudaFree(ctx->d_work);
     ctx->d_work = nullptr;
     ctx->d_work_bytes = 0;
@@ -265,6 +299,7 @@ void ccl_ctx_destroy(ccl_ctx* c) {
     if (c->d_lab) cudaFree(c->d_lab);
     if (c->h_img) cudaFreeHost(c->h_img);
     if (c->h_lab) cudaFreeHost(c->h_lab);
+    for (auto& gr : c->graphs) cudaGraphExecDestroy(gr.exec);
     if (c->d_work) cudaFree(c->d_work);
     if (c->d_metrics) cudaFree(c->d_metrics);
     if (c->d_aux) cudaFree(c->d_aux);
@@ -285,9 +320,42 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
     cclk::LaunchArgs a{};
     if (ccl_status s = make_geo(w, h, 0, img_pitch, img_pitch * h, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
     if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, 1))) return s;
+    if (!sync && graphs_enabled()) {
+        // repeated calls on the same buffers replay one CUDA graph of the
+        // (PDL-chained) launches: no per-call host work between the kernels
+        for (auto& gr : ctx->graphs)
+            if (gr.img == d_img && gr.pitch == img_pitch && gr.w == w && gr.h == h && gr.lab == d_labels &&
+                gr.variant == variant && gr.work == ctx->d_work)
+                return launch_graph(ctx, gr.exec, st);
+    }
+    if (ccl_status s = prepare(&a, d_img, img_pitch, img_pitch * h, 1, d_labels, variant, st)) return s;
     a.work = static_cast<uint32_t*>(ctx->d_work);
+    if (!sync && graphs_enabled()) {
+        // capture on the context's own stream (the legacy default stream cannot be captured)
+        cclk::LaunchArgs c = a;
+        c.stream = ctx->stream;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+            // no context events inside the graph: they would no longer be usable
+            // by later timed calls (this path reads no timing)
+            const ccl_status s = run_pipeline(ctx, c, false, false);
+            const cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+            if (s == CCL_OK && e == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                cudaGraphDestroy(graph);
+                if (ctx->graphs.size() >= 8) {
+                    cudaGraphExecDestroy(ctx->graphs.front().exec);
+                    ctx->graphs.erase(ctx->graphs.begin());
+                }
+                ctx->graphs.push_back({d_img, img_pitch, w, h, d_labels, variant, ctx->d_work, exec});
+                return launch_graph(ctx, exec, st);
+            }
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();  // capture failed: launch directly below
+        }
+    }
     if (ccl_status s = run_pipeline(ctx, a, true, sync != 0)) return s;
     if (sync) return read_timing(ctx, timing);
     return CCL_OK;

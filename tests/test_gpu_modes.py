@@ -209,3 +209,28 @@ def test_label_strips_errors(ccl):
     th = ccl.tile_shape()[1]
     with pytest.raises(ValueError):  # more strips than tile rows
         ccl.label_strips(np.ones((th, 50), np.uint8), [0, 0])
+
+
+def test_device_path_graph_replay(ccl, oracle_mod):
+    """Repeated ccl_label_device calls on the same buffers replay a cached CUDA
+    graph: new image content in the same buffer, then other buffers / shapes."""
+    import torch
+    w, h = 700, 500
+    img = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    out = torch.empty((h, w), dtype=torch.uint32, device="cuda")
+    for seed in range(4):  # same pointers every call: capture once, then replays
+        a = ccl.random_image(w, h, 0.45 + 0.05 * seed, seed)
+        img.copy_(torch.from_numpy(a))
+        ccl.label_device(img, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle_mod.sequential_ccl(a)), seed
+    for (ww, hh) in [(300, 200), (w, h)]:  # other buffers / shape, then the first graph again
+        a = ccl.random_image(ww, hh, 0.6, ww)
+        got = ccl.label_device(torch.from_numpy(a).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), oracle_mod.sequential_ccl(a))
+    a = ccl.pattern_image("spiral", w, h)
+    img.copy_(torch.from_numpy(a))
+    ccl.label_device(img, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle_mod.sequential_ccl(a))
