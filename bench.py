@@ -103,8 +103,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(img_np, max_seconds=20.0):
     """Reference CPU labeler on the host cores (oracle/_ref) — reported baseline only."""
+    import numpy as np
     import oracle
     n = os.cpu_count() or 1
     try:
@@ -118,9 +129,16 @@ def cpu_baseline(img_np, max_seconds=20.0):
                 _, ms = oracle.ref_label_image(img_np, 32, 32, "c2fl", n)
                 times.append(ms)
             ms = statistics.median(times)
-            return {"value": img_np.size / (ms * 1e-3) / 1e9, "unit": "Gpixels/s", "cores": n, "kind": "reference",
-                    "sample": f"full {img_np.shape[1]}x{img_np.shape[0]} image, ccl_ref::label_image C2FL 32x32 "
-                              f"workers={n}, median of {len(times)} (RunReport.wall_time)"}
+            out = {"value": img_np.size / (ms * 1e-3) / 1e9, "unit": "Gpixels/s", "cores": n, "kind": "reference",
+                   "sample": f"full {img_np.shape[1]}x{img_np.shape[0]} image, ccl_ref::label_image C2FL 32x32 "
+                             f"workers={n}, median of {len(times)} (RunReport.wall_time)",
+                   "cpu_model": _cpu_model(), "hardware_concurrency": n}
+            # SURVEY §8d also asks for one worker: a bounded 2048-row sample of the same image
+            sub = np.ascontiguousarray(img_np[:2048])
+            _, ms1 = oracle.ref_label_image(sub, 32, 32, "c2fl", 1)
+            out["workers1"] = {"value": sub.size / (ms1 * 1e-3) / 1e9, "unit": "Gpixels/s",
+                               "sample": f"first 2048 rows ({sub.shape[1]}x{sub.shape[0]}), workers=1, 1 run"}
+            return out
     except Exception as e:  # pragma: no cover
         print(f"[bench] reference baseline failed: {e}", file=sys.stderr)
     t0 = time.perf_counter()
