@@ -52,18 +52,6 @@
 #ifndef CCL_AIMG_OVERLAY
 #define CCL_AIMG_OVERLAY 1  // band kernel (a): TMA tile staged in the node table (no prefetch, -8 KB smem)
 #endif
-#ifndef CCL_EHALF
-#define CCL_EHALF 0  // band kernel (e): two lanes per band, 8 warps per CTA
-#endif
-#ifndef CCL_EMINB2
-#define CCL_EMINB2 4  // min resident CTAs of the 8-warp band kernel (e) (caps registers at 64)
-#endif
-#ifndef CCL_ERESOLVE
-#define CCL_ERESOLVE 0  // band mode: kernel (d2) runs as a fifth warp of kernel (e)
-#endif
-#ifndef CCL_ERES_Q
-#define CCL_ERES_Q 4  // CCL_ERESOLVE: finds per lane of the resolver warp in lockstep
-#endif
 #ifndef CCL_BAND
 #define CCL_BAND 1  // C2FL kernel (a) on 2-row band runs
 #endif

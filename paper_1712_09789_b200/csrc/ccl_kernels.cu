@@ -44,7 +44,6 @@ struct Cfg {
     static constexpr int WX = WX_, WY = WY_;  // warps across / down the tile
     static constexpr int WPL = WPL_;          // 32-px row words per lane
     static constexpr int RPL = RPL_;          // rows per lane (2: a lane owns a 2-row band)
-    static constexpr bool HALF = false;       // band kernel (e) only: two lanes per band (BandE2Cfg)
     static constexpr int WPR = WX * WPL;      // row words per tile row
     static constexpr int TW = 32 * WPR, TH = 32 * RPL * WY, NT = 32 * WX * WY, NWARP = WX * WY;
     static constexpr int PX = TW * TH;
@@ -85,16 +84,6 @@ using BandECfg = Cfg<TileCfg::WPR, TileCfg::TH / 64, 1, 2>;
 static_assert(BandCfg::TW == TileCfg::TW && BandCfg::TH == TileCfg::TH && BandCfg::TILE_WORDS == TileCfg::TILE_WORDS,
               "band kernel (a) writes the same work tiles");
 static_assert(BandECfg::TILE_WORDS == TileCfg::TILE_WORDS, "band kernel (e) reads the same work tiles");
-// Band kernel (e) with two lanes per band (each fills 16 of the word's 32
-// columns in both rows): 8 warps per CTA, warp = (word column, 16-band half),
-// one 32x32 staging tile per warp -- the same staging bytes as BandECfg with
-// twice the warps to hide the shared-memory latency chains.
-struct BandE2Cfg : BandECfg {
-    static constexpr bool HALF = true;
-    static constexpr int NT = 2 * BandECfg::NT, NWARP = 2 * BandECfg::NWARP;
-};
-static_assert(ECfg::TW == TileCfg::TW && ECfg::TH == TileCfg::TH && ECfg::TILE_WORDS == TileCfg::TILE_WORDS,
-              "kernel (e) must see kernel (a)'s work tiles");
 
 // Kernel (a) shared memory, per node granularity (runs: <= PX/2 nodes).
 template <class C, bool RUNS, bool BAND = false>
@@ -140,7 +129,7 @@ struct ELayout {
     static constexpr int S1_OFF = 0;
     static constexpr int S2_OFF = S1_OFF + 3 * S1;
     static constexpr int STG_OFF = ((S2_OFF + 2 * S2) + 1023) / 1024 * 1024;
-    static constexpr int BAR_OFF = STG_OFF + (C::HALF ? C::NWARP * 4096 : C::NWARP * C::WPL * C::RPL * 4096);
+    static constexpr int BAR_OFF = STG_OFF + C::NWARP * C::WPL * C::RPL * 4096;
     static constexpr int SMEM = BAR_OFF + 64 + 1024;
 };
 
@@ -1329,45 +1318,6 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
     metrics_phase(g, 2, mc);
 }
 
-// Kernel (d2) inside kernel (e) (CCL_ERESOLVE, band mode): the final label of
-// each of tile tt's nf seam roots into the shared-memory list FT, two finds per
-// lane climbing in lockstep (their L2 loads overlap).
-template <class C>
-__device__ __forceinline__ void resolve_tile(const Forest& fst, uint32_t tt, uint32_t nf, uint32_t* FT, int lane) {
-    constexpr int Q = CCL_ERES_Q;  // finds per lane in lockstep
-    const uint32_t base = tt * uint32_t(C::MAXF);
-    for (uint32_t k0 = lane; k0 < nf; k0 += 32 * Q) {
-        uint32_t x[Q];
-        uint2 v[Q];
-        bool c[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            const uint32_t k = k0 + 32u * q;
-            x[q] = base + (k < nf ? k : k0);
-            v[q] = fst.node(x[q]);
-        }
-        bool any = true;
-        while (any) {
-            any = false;
-#pragma unroll
-            for (int q = 0; q < Q; ++q) c[q] = v[q].x != x[q];
-            uint2 n[Q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q) n[q] = c[q] ? fst.node(v[q].x) : v[q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                if (c[q]) {
-                    x[q] = v[q].x;
-                    v[q] = n[q];
-                    any |= v[q].x != x[q];
-                }
-        }
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-            if (k0 + 32u * q < nf) FT[k0 + 32u * q] = v[q].y;
-    }
-}
-
 // ------------------------------------------------------------------ kernel (e)
 // Persistent, 3-stage pipeline per CTA: while tile i is expanded, the node
 // table + resolved seam labels of tile i+1 and the head/masks of tile i+2 are
@@ -1375,7 +1325,7 @@ __device__ __forceinline__ void resolve_tile(const Forest& fst, uint32_t tt, uin
 // swizzled staging tile and writes it with one TMA store: every label is
 // written exactly once and the image is never re-read.
 template <class C, bool RUNS, bool TMA_ST, bool BAND>
-__global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::HALF ? CCL_EMINB2 : CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+__global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
                                                     const uint32_t* work, Geo g, uint32_t ntiles) {
     using E = ELayout<C, RUNS, BAND>;
     uint8_t* smem = aligned_smem();
@@ -1391,11 +1341,8 @@ __global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::
         mbar_expect_tx(&b1[j], E::S1B);
         bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), E::S1B, &b1[j]);
     };
-    // band mode with CCL_ERESOLVE: warp NWARP resolves the seam labels of the
-    // next tile into its stage (no kernel (d2)); the copies bring the table only
-    constexpr bool RES = BAND && CCL_ERESOLVE;
     auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
-        const uint32_t lb = RES ? 0u : (head[0] * 4 + 15) & ~15u;
+        const uint32_t lb = (head[0] * 4 + 15) & ~15u;
         const uint32_t tb = head[1] <= uint32_t(E::TBLN) ? (head[1] * 2 + 15) & ~15u : 0u;
         const uint32_t* wt = work_tile<C>(const_cast<uint32_t*>(work), t);
         mbar_expect_tx(&b2[j], lb + tb);
@@ -1405,7 +1352,7 @@ __global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::
     if (tid == 0 && TMA_ST) prefetch_tmap(&tm_lab);
     if (tid == 0) {
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
-        for (int j = 0; j < 2; ++j) mbar_init(&b2[j], RES ? 2 : 1);
+        for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
         const uint32_t t0 = blockIdx.x;
         // heads / masks come from kernel (a), complete before (d2) let this grid
         // launch; only the seam labels of (d2) need the dependency wait.  Every
@@ -1419,32 +1366,11 @@ __global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::
         }
     }
     __syncthreads();
-    const Forest fres = forest_of<C>(const_cast<uint32_t*>(work), ntiles);
-    if (RES && warp == C::NWARP) {  // the first tile's seam labels
-        pdl_wait();                 // the forest is final once the previous kernels are done
-        if (blockIdx.x < ntiles) {
-            mbar_wait(&b1[0], 0);
-            resolve_tile<C>(fres, blockIdx.x, s1buf(0)[0], s2buf(0), lane);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&b2[0]);
-        }
-    }
 
     const int sw = lane & 7;
     uint32_t it = 0;
     TileWalk walk(blockIdx.x, G, g);
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it, walk.advance()) {
-        if (RES && warp == C::NWARP) {  // resolver warp: the next tile's seam labels
-            if (t + G < ntiles) {
-                const uint32_t jn = (it + 1) % 3, jr = (it + 1) & 1u;
-                mbar_wait(&b1[jn], ((it + 1) / 3) & 1u);
-                resolve_tile<C>(fres, t + G, s1buf(jn)[0], s2buf(jr), lane);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&b2[jr]);
-            }
-            __syncthreads();  // pairs with the workers' end-of-tile barrier
-            continue;
-        }
         const uint32_t j1 = it % 3, j2 = it & 1u;
         if (tid == 0) {
             if (t + 2 * G < ntiles) s1(t + 2 * G, (it + 2) % 3);
@@ -1472,73 +1398,7 @@ __global__ void __launch_bounds__(C::NT + ((BAND && CCL_ERESOLVE) ? 32 : 0), C::
             __syncwarp();
         }
         uint32_t* Lf = L + size_t(ti.fz) * g.frame_px;
-        if constexpr (C::HALF) {
-            auto expand = [&](const uint16_t* tbl) {
-            // lane = (band b, half hf): rows 2b, 2b+1, columns 16 hf .. 16 hf + 15 of
-            // word column wx; this warp's 16 bands are rows 32 wy .. 32 wy + 31
-            const int bl = lane & 15, hf = lane >> 4;
-            const int b = 16 * wy + bl, wc = wx;
-            const int r0 = 2 * b, r1 = r0 + 1;
-            uint8_t* stg = smem + E::STG_OFF + warp * 4096;
-            uint8_t* row0 = stg + (r0 & 31) * 128;
-            uint8_t* row1 = stg + (r1 & 31) * 128;
-            const int sw0 = r0 & 7, sw1 = r1 & 7;
-            const uint32_t tm = M[r0 * C::WPR + wc], um = M[r1 * C::WPR + wc];
-            const uint32_t st = BSt[b * C::WPR + wc];
-            const uint32_t pfx = PF16[b * C::WPR + wc];
-            const uint32_t c0 = 16u * uint32_t(hf);                   // first column of this half
-            const uint32_t before = st & ((1u << c0) - 1u);            // starts left of this half
-            // the node covering column c0 when it does not start there
-            uint32_t cur = (!((st >> c0) & 1u) && (((tm | um) >> c0) & 1u)) ? lab_of(tbl[pfx + __popc(before) - 1]) : kBG;
-            {
-                const uint16_t* e = tbl + pfx + __popc(before);
-                uint32_t tt = st & (0xFFFFu << c0);
-                while (tt) {
-                    const uint32_t bb = __ffs(tt) - 1;
-                    tt &= tt - 1;
-                    *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(*e++);
-                }
-            }
-            uint4 vv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) vv[j] = *reinterpret_cast<const uint4*>(row0 + (((4 * hf + j) ^ sw0) << 4));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = 4 * hf + j;
-                uint4* p0 = reinterpret_cast<uint4*>(row0 + ((c ^ sw0) << 4));
-                uint4* p1 = reinterpret_cast<uint4*>(row1 + ((c ^ sw1) << 4));
-                const uint4 v = vv[j];
-                uint32_t a[4] = {v.x, v.y, v.z, v.w}, a1[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = 4 * c + q;
-                    cur = ((st >> i) & 1u) ? a[q] : cur;
-                    a[q] = ((tm >> i) & 1u) ? cur : kBG;
-                    a1[q] = ((um >> i) & 1u) ? cur : kBG;
-                }
-                if (TMA_ST) {
-                    *p0 = make_uint4(a[0], a[1], a[2], a[3]);
-                    *p1 = make_uint4(a1[0], a1[1], a1[2], a1[3]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t gx = x0 + wc * 32 + 4 * c + q;
-                        if (gx < g.W && y0 + r0 < g.H) Lf[size_t(y0 + r0) * g.W + gx] = a[q];
-                        if (gx < g.W && y0 + r1 < g.H) Lf[size_t(y0 + r1) * g.W + gx] = a1[q];
-                    }
-                }
-            }
-            if (TMA_ST) {
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0)
-                    tma_store_3d_hint(&tm_lab, int(x0 + wc * 32), int(y0 + 32 * wy), int(ti.fz), stg,
-                                      policy_evict_first());
-            }
-            };
-            if (M[-4 + 1] <= uint32_t(E::TBLN)) expand(TBL);
-            else expand(reinterpret_cast<const uint16_t*>(work_tile<C>(const_cast<uint32_t*>(work), t) + C::W_TBL));
-        } else if constexpr (C::RPL == 2) {
+        if constexpr (C::RPL == 2) {
             // (a lambda called once per table location, so the shared-memory
             // table keeps LDS and the global fallback uses LDG)
             auto expand = [&](const uint16_t* tbl) {
@@ -1798,18 +1658,13 @@ cudaError_t launch_local(const LaunchArgs& a) {
 
 template <bool RUNS, bool BAND>
 static cudaError_t launch_final_v(const LaunchArgs& a) {
-    using BE = typename std::conditional<CCL_EHALF != 0, BandE2Cfg, BandECfg>::type;
-    using C = typename std::conditional<BAND, BE, ECfg>::type;
+    using C = typename std::conditional<BAND, BandECfg, ECfg>::type;
     using E = ELayout<C, RUNS, BAND>;
     const uint32_t nt = tile_count(a);
-    constexpr bool RES = BAND && CCL_ERESOLVE;  // (d2) runs inside (e)
-    constexpr int NTH = C::NT + (RES ? 32 : 0);
-    cudaError_t e = cudaSuccess;
-    if (!RES) {
-        e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream, a.work,
-                       a.g, nt);
-        if (e != cudaSuccess) return e;
-    }
+    constexpr int NTH = C::NT;
+    cudaError_t e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream,
+                               a.work, a.g, nt);
+    if (e != cudaSuccess) return e;
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
