@@ -71,6 +71,14 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
  * Blocking.  `kernel_ms` (may be NULL) = device time of the kernels only. */
 ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels,
                           int variant, float* kernel_ms);
+/* The same, asynchronous: H2D, kernels and D2H are enqueued on ctx's stream
+ * and the call returns at once; img / labels must stay valid (and should be
+ * page-locked for the copies to overlap) until ccl_ctx_sync(ctx).  A caller
+ * alternating two contexts overlaps an image's upload with the previous
+ * image's label download. */
+ccl_status ccl_label_host_async(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels,
+                                int variant);
+ccl_status ccl_ctx_sync(ccl_ctx* ctx);
 
 /* Batch of n frames of w*h, frame f at d_frames + f*frame_pitch (rows of
  * img_pitch bytes).  Labels are per-frame raster indices at d_labels + f*w*h.

@@ -73,6 +73,8 @@ _sig("ccl_ctx_destroy", None, _vp)
 _sig("ccl_ctx_stream", _vp, _vp)
 _sig("ccl_label_device", _c, _vp, _vp, _sz, _u32, _u32, _vp, _c, _vp, _c, ctypes.POINTER(_Timing))
 _sig("ccl_label_host", _c, _vp, _u8p, _u32, _u32, _u32p, _c, ctypes.POINTER(ctypes.c_float))
+_sig("ccl_label_host_async", _c, _vp, _u8p, _u32, _u32, _u32p, _c)
+_sig("ccl_ctx_sync", _c, _vp)
 _sig("ccl_label_batch", _c, _vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _c, _vp)
 _sig("ccl_strip_local", _c, _vp, _vp, _sz, _u32, _u32, _u32, _u32, _vp, _vp, _c, _vp)
 _sig("ccl_strip_seam_export", _c, _vp, _u32, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _vp)
@@ -99,6 +101,7 @@ _sig("ccl_version", ctypes.c_char_p)
 
 C_ABI_SYMBOLS = [
     "ccl_ctx_create", "ccl_ctx_destroy", "ccl_ctx_stream", "ccl_label_device", "ccl_label_host", "ccl_label_batch",
+    "ccl_label_host_async", "ccl_ctx_sync",
     "ccl_gen_random_device", "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",

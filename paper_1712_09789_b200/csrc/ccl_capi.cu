@@ -380,6 +380,27 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
 
 ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels, int variant,
                           float* kernel_ms) {
+    if (ccl_status s = ccl_label_host_async(ctx, img, w, h, labels, variant)) return s;
+    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
+    ccl_timing t{};
+    if (ccl_status s = read_timing(ctx, &t)) return s;
+    if (kernel_ms) *kernel_ms = t.total_ms;
+    return CCL_OK;
+}
+
+ccl_status ccl_ctx_sync(ccl_ctx* ctx) {
+    if (!ctx) return fail(CCL_EINVAL, "null context");
+    DeviceGuard dg(ctx->device);
+    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
+    return CCL_OK;
+}
+
+// H2D, kernels and D2H enqueued on the context's stream; returns at once.
+// With page-locked img / labels the copies are asynchronous, so a caller that
+// alternates two contexts overlaps one image's upload with the previous
+// image's label download (PCIe is full duplex).
+ccl_status ccl_label_host_async(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels,
+                                int variant) {
     if (!ctx || !img || !labels) return fail(CCL_EINVAL, "null argument");
     if (ccl_status s = check_dims(w, h)) return s;
     if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
@@ -401,13 +422,9 @@ ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t
         ctx->d_lab_bytes = lab_bytes;
     }
     CCL_CHECK(cudaMemcpy2DAsync(ctx->d_img, pitch, img, w, w, h, cudaMemcpyHostToDevice, ctx->stream));
-    ccl_timing t{};
     if (ccl_status s = ccl_label_device(ctx, ctx->d_img, pitch, w, h, ctx->d_lab, variant, ctx->stream, 0, nullptr))
         return s;
     CCL_CHECK(cudaMemcpyAsync(labels, ctx->d_lab, lab_bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    CCL_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (ccl_status s = read_timing(ctx, &t)) return s;
-    if (kernel_ms) *kernel_ms = t.total_ms;
     return CCL_OK;
 }
 

@@ -234,3 +234,28 @@ def test_device_path_graph_replay(ccl, oracle_mod):
     ccl.label_device(img, out)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle_mod.sequential_ccl(a))
+
+
+def test_label_host_async_two_contexts(ccl, oracle_mod):
+    """ccl_label_host_async + ccl_ctx_sync: a stream of host images on two
+    alternating contexts (pinned buffers), every result bit-exact."""
+    import ctypes
+    import torch
+    w, h = 640, 480
+    imgs = [ccl.random_image(w, h, 0.4 + 0.05 * k, k) for k in range(5)]
+    hin = [torch.from_numpy(a).pin_memory() for a in imgs]
+    hout = [torch.empty((h, w), dtype=torch.int32).pin_memory() for _ in imgs]
+    ctxs = [ccl.Context(0), ccl.Context(0)]
+    for k in range(len(imgs)):
+        c = ctxs[k & 1]
+        if k >= 2:
+            ccl._check(ccl._lib.ccl_ctx_sync(c.handle))
+            done = hout[k - 2].numpy().view(np.uint32)
+            assert np.array_equal(done, oracle_mod.sequential_ccl(imgs[k - 2])), k - 2
+        ccl._check(ccl._lib.ccl_label_host_async(
+            c.handle, ctypes.cast(hin[k].data_ptr(), ccl._u8p), w, h,
+            ctypes.cast(hout[k].data_ptr(), ccl._u32p), 0))
+    for c in ctxs:
+        ccl._check(ccl._lib.ccl_ctx_sync(c.handle))
+    for k in (len(imgs) - 2, len(imgs) - 1):
+        assert np.array_equal(hout[k].numpy().view(np.uint32), oracle_mod.sequential_ccl(imgs[k])), k
