@@ -345,7 +345,7 @@ __device__ __forceinline__ uint32_t tile_prefix(uint32_t cnt, uint32_t* CNT, uin
 // Id of the node holding bit b of a word with starts st and prefix pfx (a bit
 // before the word's first start belongs to the node continuing from the left).
 __device__ __forceinline__ uint32_t node_of(uint32_t pfx, uint32_t st, uint32_t b) {
-    return pfx + __popc(st & (0xFFFFFFFFu >> (31u - b))) - 1u;
+    return pfx + __popc(st << (31u - b)) - 1u;  // the starts at or below bit b
 }
 // Bits b of o such that some bit of o lies strictly below b inside the same
 // run of m (o must be a subset of m): the carry-in vector of m + o, within m.
