@@ -1009,11 +1009,11 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 while (tt) {
                     const uint32_t f = __ffs(tt) - 1;
                     tt &= tt - 1;
-                    const uint32_t nxt = tt ? __ffs(tt) - 1 : 32u;
-                    const uint32_t gg = ff ? __ffs(ff) - 1 : 32u;
                     uint32_t v = kRoot | (rowpos0 + f);
-                    if (gg < nxt) {
-                        v = node_of(upfx[k], ubs[k], gg);
+                    // lowest overlap before the next run's first top pixel (an empty
+                    // mask's isolated low bit - 1 wraps to "infinity")
+                    if ((ff & (0u - ff)) - 1u < (tt & (0u - tt)) - 1u) {
+                        v = node_of(upfx[k], ubs[k], __ffs(ff) - 1);
                         ff &= ff - 1;
                     }
                     P[node_of(pfx[k], bs[k], f)] = node_t(v);
@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 if (code & kSeam) v = FR[1 + (code & kCode)];
             }
             wt[C::W_REC + i] = v;
-            if (i < 2 * C::TW) {
+            if ((edge_top || edge_bot) && i < 2 * C::TW) {  // strip-edge tiles only
                 const bool top = i < C::TW;
                 const uint32_t gx = x0 + (top ? i : i - C::TW);
                 if ((top ? edge_top : edge_bot) && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
