@@ -1104,8 +1104,11 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         const bool has_top = ty > 0 || g.edge_above;
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
-        for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
-            const bool act = i < C::TW ? has_top : i < 2 * C::TW ? has_bot : i < 2 * C::TW + C::TH ? has_left : has_right;
+        static_assert(C::NT == C::TW && C::NT == 2 * C::TH, "one top, one bottom and one side item per thread");
+#pragma unroll
+        for (int s3 = 0; s3 < 3; ++s3) {
+            const int i = s3 * C::NT + tid;  // top, bottom, then left / right
+            const bool act = s3 == 0 ? has_top : s3 == 1 ? has_bot : (tid < C::TH ? has_left : has_right);
             uint32_t x = BN[i];
             if (!act || x == 0xFFFFu) continue;
             uint32_t p = P[x];
@@ -1158,7 +1161,9 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         CCL_PH(13);
         // ---- seam records + strip-edge rows
         const bool edge_top = ty == 0 && g.edge_above, edge_bot = ty + 1 == g.nty && g.edge_below;
-        for (int i = tid; i < 2 * C::TW + 2 * C::TH; i += C::NT) {
+#pragma unroll
+        for (int s3 = 0; s3 < 3; ++s3) {
+            const int i = s3 * C::NT + tid;  // top, bottom, then left / right
             const uint32_t x = BN[i];
             uint32_t v = kBG;
             if (x != 0xFFFFu) {
@@ -1166,10 +1171,9 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 if (code & kSeam) v = FR[1 + (code & kCode)];
             }
             wt[C::W_REC + i] = v;
-            if ((edge_top || edge_bot) && i < 2 * C::TW) {  // strip-edge tiles only
-                const bool top = i < C::TW;
-                const uint32_t gx = x0 + (top ? i : i - C::TW);
-                if ((top ? edge_top : edge_bot) && gx < g.W) SE[(top ? 0u : g.W) + gx] = v;
+            if (s3 < 2 && (s3 == 0 ? edge_top : edge_bot)) {  // strip-edge tiles only
+                const uint32_t gx = x0 + uint32_t(tid);
+                if (gx < g.W) SE[(s3 == 0 ? 0u : g.W) + gx] = v;
             }
         }
 #if CCL_FUSE_SEAMS
