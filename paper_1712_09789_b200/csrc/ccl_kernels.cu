@@ -867,7 +867,9 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
         CCL_PH(8);
-        for (int i = tid; i < A::MAXN / 32; i += C::NT) FB[i] = 0u;
+#pragma unroll
+        for (int k = 0; k < (A::MAXN / 32 + C::NT - 1) / C::NT; ++k)  // fixed trip count (tid < NT)
+            if (k * C::NT + tid < A::MAXN / 32) FB[k * C::NT + tid] = 0u;
         if (tid == 0) FR[0] = 0u;
 
         // ---- row-word foreground masks (byte == 1)
@@ -876,7 +878,9 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             constexpr int CPR = C::TW / 16;
             uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
 #pragma unroll
-            for (int c = tid; c < C::TH * CPR; c += C::NT) {
+            static_assert((C::TH * CPR) % C::NT == 0, "whole mask-build rounds");
+            for (int kk = 0; kk < C::TH * CPR / C::NT; ++kk) {
+                const int c = kk * C::NT + tid;
                 const uint4 q = *reinterpret_cast<const uint4*>(IMG + c * 16);
                 M16[c] = static_cast<uint16_t>(eq1_mask16(q));
             }
