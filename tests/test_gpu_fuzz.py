@@ -13,7 +13,7 @@ VARIANTS = ["c2fl", "rc2fl", "cc2fl", "nc2fl"]
 
 
 @pytest.mark.gpu
-@settings(max_examples=int(os.environ.get("CCL_FUZZ_EXAMPLES", "120")), deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@settings(max_examples=int(os.environ.get("CCL_FUZZ_EXAMPLES", "300")), deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(w=st.integers(1, 700), h=st.integers(1, 300), density=st.floats(0.0, 1.0), seed=st.integers(0, 2**31),
        variant=st.sampled_from(VARIANTS), junk=st.booleans(), pad=st.integers(0, 37))
 def test_random_images(ccl, oracle_mod, w, h, density, seed, variant, junk, pad):
