@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <string>
 
 #include "ccl/errors.hpp"
@@ -27,6 +28,13 @@ LabelMapFormat parse_label_format(const std::string& s);  // std::invalid_argume
 void write_label_map(const LabelMap& lm, const std::string& path, LabelMapFormat format);
 
 LabelMap read_label_map(const std::string& path);  // compacted map from a CCLM file
+
+// Per-block counter grids ("iterations", then "atomics", one CSV row per block
+// row) and the summary row width,height,block_w,block_h,density,variant,
+// mean_iterations,mean_atomics,wall_ms (density empty when unknown; no summary
+// row for an empty report) -- reference label_io.hpp / label_io.cpp:97-128.
+void write_metrics_csv(const RunReport& report, const std::string& path,
+                       std::optional<double> density = std::nullopt);
 
 // Labels `img` on the calling thread's GPU and writes the compacted map as a
 // CCLM file; returns the number of components K.

@@ -16,28 +16,14 @@
 #include <string>
 #include <vector>
 
+#include "ccl/forest.hpp"
 #include "ccl/image.hpp"
 
 namespace ccl {
 
-// Per-block cost counters (forest.hpp:15-29).  The GPU path does not
-// reproduce the CPU's find-root / CAS counts; per_block is sized and
-// block_id-numbered exactly as the reference, counters stay 0.
-struct BlockMetrics {
-    std::uint32_t block_id = 0;
-    std::uint64_t findroot_iterations = 0;
-    std::uint64_t atomic_ops = 0;
-
-    void reset() {
-        findroot_iterations = 0;
-        atomic_ops = 0;
-    }
-    BlockMetrics& operator+=(const BlockMetrics& o) {
-        findroot_iterations += o.findroot_iterations;
-        atomic_ops += o.atomic_ops;
-        return *this;
-    }
-};
+// BlockMetrics (reference forest.hpp:15-29) comes from ccl/forest.hpp, included
+// here as the reference pipeline.hpp:7 does.  The product build leaves its
+// counters 0; the instrumented build fills them per GPU tile.
 
 // pipeline.hpp:15-26
 struct RunReport {

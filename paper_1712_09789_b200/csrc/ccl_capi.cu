@@ -237,7 +237,9 @@ ccl_status read_timing(ccl_ctx* ctx, ccl_timing* t) {
     return CCL_OK;
 }
 
-ccl_status ensure_work(ccl_ctx* ctx, size_t bytes) {
+// Grows the context's work buffer; the zero fill is ordered on the stream of
+// the call that uses the buffer next.
+ccl_status ensure_work(ccl_ctx* ctx, size_t bytes, cudaStream_t st) {
     if (ctx->d_work_bytes >= bytes) return CCL_OK;
     for (auto& gr : ctx->graphs) cudaGraphExecDestroy(gr.exec);  // they point at the old buffer
     ctx->graphs.clear();
@@ -245,7 +247,7 @@ ccl_status ensure_work(ccl_ctx* ctx, size_t bytes) {
     ctx->d_work = nullptr;
     ctx->d_work_bytes = 0;
     CCL_CHECK(cudaMalloc(&ctx->d_work, bytes));
-    CCL_CHECK(cudaMemset(ctx->d_work, 0, bytes));  // seam flags start clear
+    CCL_CHECK(cudaMemsetAsync(ctx->d_work, 0, bytes, st));  // seam flags start clear
     ctx->d_work_bytes = bytes;
     return CCL_OK;
 }
@@ -321,7 +323,7 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
     if (ccl_status s = make_geo(w, h, 0, img_pitch, img_pitch * h, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
-    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, 1))) return s;
+    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, 1), static_cast<cudaStream_t>(stream))) return s;
     if (!sync && graphs_enabled()) {
         // repeated calls on the same buffers replay one CUDA graph of the
         // (PDL-chained) launches: no per-call host work between the kernels
@@ -373,7 +375,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ccl_status s = prepare(&a, d_frames, img_pitch, frame_pitch, n, d_labels, variant, st)) return s;
-    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, n))) return s;
+    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, n), st)) return s;
     a.work = static_cast<uint32_t*>(ctx->d_work);
     return run_pipeline(ctx, a, true);
 }

@@ -32,6 +32,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "ccl_device.cuh"
@@ -1549,33 +1552,27 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
 }
 
 // ================================================================== host side
-// Persistent grid: every SM filled to the kernel's occupancy (cached per device).
+// Persistent grid: every SM filled to the kernel's occupancy, cached per
+// (kernel, device, block, smem) -- each template instantiation has its own
+// entry -- under a mutex (strip workers call this from several host threads).
 template <class K>
-static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles, int slot) {
-    static int cache[64][8];
+static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, int>, int> cache;
     int dev = 0;
     cudaGetDevice(&dev);
-    int& per = cache[dev & 63][slot];
-    if (per == 0) {
-        int n = 0, sms = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        per = (n > 0 ? n : 1) * (sms > 0 ? sms : 1);
-    }
-    return unsigned(per < int(ntiles) ? per : int(ntiles));
-}
-
-template <class K>
-static unsigned persistent_grid_x(K kernel, int threads, int smem, uint32_t ntiles, int slot) {
-    static int cache[64][4];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int& per = cache[dev & 63][slot];
-    if (per == 0) {
-        int n = 0, sms = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        per = (n > 0 ? n : 1) * (sms > 0 ? sms : 1);
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, threads, smem);
+    int per;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            int n = 0, sms = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            it = cache.emplace(key, (n > 0 ? n : 1) * (sms > 0 ? sms : 1)).first;
+        }
+        per = it->second;
     }
     return unsigned(per < int(ntiles) ? per : int(ntiles));
 }
@@ -1620,13 +1617,13 @@ static cudaError_t launch_local_v(const LaunchArgs& a) {
         auto k = k_local<C, VAR, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        const cudaError_t e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, VAR)), C::NT, A::SMEM,
+        const cudaError_t e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt)), C::NT, A::SMEM,
                                         a.stream, false, a.tm_img, a.img, a.labels, a.work, a.g, nt);
         if (e != cudaSuccess) return e;
     } else {
         auto k = k_local<C, VAR, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
-        k<<<persistent_grid(k, C::NT, A::SMEM, nt, 4 + VAR), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
+        k<<<persistent_grid(k, C::NT, A::SMEM, nt), C::NT, A::SMEM, a.stream>>>(a.tm_img, a.img, a.labels,
                                                                                            a.work, a.g, nt);
     }
     return cudaGetLastError();
@@ -1643,12 +1640,12 @@ static cudaError_t launch_local_band(const LaunchArgs& a) {
         auto k = k_local_band<C, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt, 6), nt)), C::NT, A::SMEM, a.stream, false,
+        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt), nt)), C::NT, A::SMEM, a.stream, false,
                       a.tm_img, a.img, a.work, a.g, nt);
     } else {
         auto k = k_local_band<C, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
-        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, 7)), C::NT, A::SMEM, a.stream, false, a.tm_img,
+        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt)), C::NT, A::SMEM, a.stream, false, a.tm_img,
                       a.img, a.work, a.g, nt);
     }
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -1677,12 +1674,12 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
         auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, NTH, E::SMEM, nt, BAND ? 2 : (RUNS ? 0 : 1))), NTH, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid(k, NTH, E::SMEM, nt)), NTH, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
         auto k = k_final<C, RUNS, false, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
-        e = launch_pdl(k, dim3(persistent_grid_x(k, NTH, E::SMEM, nt, BAND ? 3 : (RUNS ? 0 : 1))), NTH, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid(k, NTH, E::SMEM, nt)), NTH, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     }
     return e != cudaSuccess ? e : cudaGetLastError();

@@ -99,6 +99,31 @@ LabelMap read_label_map(const std::string& path) {
     return lm;
 }
 
+// Reference label_io.cpp:97-128: the counter grids of aggregate_metrics, then
+// one summary row (none for an empty report).
+void write_metrics_csv(const RunReport& report, const std::string& path, std::optional<double> density) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw IoError("cannot open " + path + " for writing");
+    const MetricsSummary s = aggregate_metrics(report);
+    for (const auto* grid : {&s.iterations_grid, &s.atomics_grid}) {
+        os << (grid == &s.iterations_grid ? "iterations" : "atomics") << '\n';
+        for (std::uint32_t by = 0; by < s.grid_h; ++by) {
+            for (std::uint32_t bx = 0; bx < s.grid_w; ++bx)
+                os << (bx ? "," : "") << (*grid)[std::size_t(by) * s.grid_w + bx];
+            os << '\n';
+        }
+    }
+    os << "width,height,block_w,block_h,density,variant,mean_iterations,mean_atomics,wall_ms\n";
+    if (!report.per_block.empty()) {
+        os << report.label_map.width << ',' << report.label_map.height << ',' << report.cfg.block_w << ','
+           << report.cfg.block_h << ',';
+        if (density) os << *density;
+        os << ',' << to_string(report.variant) << ',' << s.mean_iterations << ',' << s.mean_atomics << ','
+           << report.wall_time.count() << '\n';
+    }
+    if (!os) throw IoError("write failed: " + path);
+}
+
 }  // namespace ccl
 
 // ------------------------------------------------------------------ C-ABI

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "ccl/generate.hpp"
@@ -47,6 +48,34 @@ void check(ccl_status s) {
     if (s == CCL_EINVAL) throw std::invalid_argument(ccl_last_error());
     if (s != CCL_OK) throw DeviceError(int(s), ccl_last_error());
 }
+
+void cuda_check(cudaError_t e, const char* where) {
+    if (e != cudaSuccess)
+        throw DeviceError(e == cudaErrorMemoryAllocation ? CCL_ENOMEM : CCL_ECUDA,
+                          std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Makes `dev` current for the scope (restores the caller's device after).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Device allocation freed on scope exit (also when a later step throws).
+struct DeviceBuffer {
+    void* p = nullptr;
+    explicit DeviceBuffer(std::size_t bytes) { cuda_check(cudaMalloc(&p, bytes), "cudaMalloc"); }
+    ~DeviceBuffer() { cudaFree(p); }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
 
 }  // namespace
 
@@ -165,6 +194,9 @@ std::vector<LabelMap> label_batch(const std::vector<BinaryImage>& frames, Varian
     for (const auto& f : frames)
         if (f.width != w || f.height != h) throw std::invalid_argument("label_batch: frames differ in size");
     ccl_ctx* ctx = thread_ctx();
+    // the staging buffers live on the context's device, not on whatever device
+    // the calling thread happens to have current
+    DeviceScope on(t_device);
     const std::size_t px = BinaryImage::check_size(w, h);
     const std::size_t pitch = (std::size_t(w) + 15) / 16 * 16, fpitch = pitch * h;
     const std::uint32_t n = std::uint32_t(frames.size());
@@ -172,32 +204,19 @@ std::vector<LabelMap> label_batch(const std::vector<BinaryImage>& frames, Varian
     for (std::uint32_t f = 0; f < n; ++f)
         for (std::uint32_t y = 0; y < h; ++y)
             std::copy_n(frames[f].data.data() + std::size_t(y) * w, w, host.data() + f * fpitch + y * pitch);
-    std::uint8_t* d_img = nullptr;
-    std::uint32_t* d_lab = nullptr;
-    if (cudaMalloc(&d_img, host.size()) != cudaSuccess) throw DeviceError(CCL_ENOMEM, "cudaMalloc frames");
-    if (cudaMalloc(&d_lab, px * n * 4) != cudaSuccess) {
-        cudaFree(d_img);
-        throw DeviceError(CCL_ENOMEM, "cudaMalloc labels");
-    }
-    auto cleanup = [&] {
-        cudaFree(d_img);
-        cudaFree(d_lab);
-    };
+    DeviceBuffer d_img(host.size()), d_lab(px * n * 4);
     cudaStream_t st = static_cast<cudaStream_t>(ccl_ctx_stream(ctx));
-    cudaMemcpyAsync(d_img, host.data(), host.size(), cudaMemcpyHostToDevice, st);
-    const ccl_status s = ccl_label_batch(ctx, d_img, pitch, fpitch, n, w, h, d_lab, int(variant), st);
-    if (s != CCL_OK) {
-        cleanup();
-        check(s);
-    }
+    cuda_check(cudaMemcpyAsync(d_img.p, host.data(), host.size(), cudaMemcpyHostToDevice, st), "label_batch H2D");
+    check(ccl_label_batch(ctx, static_cast<std::uint8_t*>(d_img.p), pitch, fpitch, n, w, h,
+                          static_cast<std::uint32_t*>(d_lab.p), int(variant), st));
     out.reserve(n);
     for (std::uint32_t f = 0; f < n; ++f) {
         out.emplace_back(w, h);
-        cudaMemcpyAsync(out.back().labels.data(), d_lab + f * px, px * 4, cudaMemcpyDeviceToHost, st);
+        cuda_check(cudaMemcpyAsync(out.back().labels.data(), static_cast<std::uint32_t*>(d_lab.p) + f * px, px * 4,
+                                   cudaMemcpyDeviceToHost, st),
+                   "label_batch D2H");
     }
-    const cudaError_t e = cudaStreamSynchronize(st);
-    cleanup();
-    if (e != cudaSuccess) throw DeviceError(CCL_ECUDA, cudaGetErrorString(e));
+    cuda_check(cudaStreamSynchronize(st), "label_batch");
     return out;
 }
 

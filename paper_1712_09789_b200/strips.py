@@ -68,11 +68,13 @@ class StripLabeler:
                                     out.data_ptr(), self.work.data_ptr(), v, s))
         _check(_lib.ccl_strip_seam_export(c, self.w, self.h, self.row0, self.full_h, self.rank, out.data_ptr(),
                                           self.work.data_ptr(), self.seam.data_ptr(), s))
-        if stream is not None:
+        if stream is not None and not isinstance(stream, int):
             with torch.cuda.stream(stream):
                 allseams = exchange_seams(self.seam, self.world, self.group)
         else:
             allseams = exchange_seams(self.seam, self.world, self.group)
+            if stream is not None:  # raw stream handle: keep the gather alive until it has run
+                torch.cuda.current_stream().synchronize()
         _check(_lib.ccl_strip_seam_resolve(c, allseams.data_ptr(), self.world, self.rank, self.w, self.h, self.row0,
                                            self.full_h, out.data_ptr(), self.work.data_ptr(), self.scratch.data_ptr(),
                                            s))
@@ -88,6 +90,11 @@ def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx
     concatenation.  Returns the (H, W) uint32 global label map."""
     import torch
     from . import _ctx
+    if stream is not None and not isinstance(stream, int):
+        # temporaries are allocated on (and freed back to) the stream the
+        # kernels run on, so the caching allocator cannot hand them out early
+        with torch.cuda.stream(stream):
+            return label_strips_single_gpu(img, n_strips, variant, None, ctx)
     h_full, w = img.shape
     ctx = ctx or _ctx(img.device.index or 0)
     v = int(Variant.parse(variant))
