@@ -89,12 +89,43 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
 /* One image over several devices in one process (the additive C++ entry point
  * ccl::label_image_strips): devices[k] labels strip k (near-equal row bands,
  * all but the last a multiple of the tile height) with the strip protocol
- * below; seams are exchanged by peer copies.  A device may be listed more than
- * once (virtual strips).  Host buffers; labels are global raster indices,
- * bit-exact with ccl_label_host.  *kernel_ms = max over strips of the device
- * time from the first kernel to the last (exchange included). */
+ * below; each strip's seam export is stored straight into every strip's
+ * exchange area (NVLink peer stores between distinct devices) and the strips'
+ * streams are ordered by cross-device events -- one host thread, no joins.
+ * A device may be listed more than once (virtual strips).  Contexts and
+ * buffers are cached for the next call with the same devices and shape.
+ * Host buffers; labels are global raster indices, bit-exact with
+ * ccl_label_host.  *kernel_ms = max over strips of the device time from the
+ * first kernel to the last (exchange included). */
 ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, uint32_t w, uint32_t h,
                             uint32_t* labels, int variant, float* kernel_ms);
+
+/* ---- Strip groups: one image over N GPUs, one process (rank) per GPU ----
+ * The seam exchange is inside the library and needs no host round trip per
+ * step: every rank owns an exchange area in its HBM, shared through a CUDA IPC
+ * handle; a rank's step stores its 16*W-byte seam export into every rank's
+ * area over NVLink and raises its epoch flag there (release, system scope);
+ * each rank's seam resolve waits on its LOCAL flags (acquire, system scope),
+ * then runs the same union-find over all N exports (no broadcast).  Setup:
+ *   1. ccl_strip_group_create on every rank -> CCL_IPC_HANDLE_BYTES of handle
+ *   2. all-gather the handles (any host channel, e.g. torch.distributed), rank order
+ *   3. ccl_strip_group_connect(group, all_handles)
+ * Then every step: ccl_strip_group_label on each rank with its strip
+ * (ccl_strip_group_rows: rows [row0, row0+h) of the full image; d_labels holds
+ * global raster indices for those rows).  Steps must be issued in the same
+ * order on all ranks.  A rank whose peers never arrive traps after 20 s. */
+typedef struct ccl_strip_group ccl_strip_group;
+#define CCL_IPC_HANDLE_BYTES 64
+size_t ccl_strip_group_handle_bytes(void);
+ccl_status ccl_strip_group_create(ccl_ctx* ctx, uint32_t rank, uint32_t n_ranks, uint32_t w, uint32_t full_h,
+                                  ccl_strip_group** out, void* handle_out);
+ccl_status ccl_strip_group_connect(ccl_strip_group* group, const void* all_handles);
+ccl_status ccl_strip_group_rows(const ccl_strip_group* group, uint32_t* row0, uint32_t* h);
+ccl_status ccl_strip_group_label(ccl_strip_group* group, const uint8_t* d_img, size_t img_pitch, uint32_t* d_labels,
+                                 int variant, void* stream);
+/* kernel launches (and copies) one ccl_strip_group_label enqueues */
+int ccl_strip_group_launches(const ccl_strip_group* group);
+void ccl_strip_group_destroy(ccl_strip_group* group);
 
 /* ---- Strip mode (image split into horizontal strips, one per GPU/rank) ----
  * A strip holds rows [row0, row0+h) of a full image of `full_h` rows, width w;

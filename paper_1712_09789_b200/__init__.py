@@ -92,6 +92,13 @@ _sig("ccl_compact_scratch_words", _sz, _u32, _u32)
 _sig("ccl_tile_shape", None, _u32p, _u32p)
 _sig("ccl_launches_per_label", _c)
 _sig("ccl_metrics_build", _c)
+_sig("ccl_strip_group_handle_bytes", _sz)
+_sig("ccl_strip_group_create", _c, _vp, _u32, _u32, _u32, _u32, ctypes.POINTER(_vp), ctypes.c_char_p)
+_sig("ccl_strip_group_connect", _c, _vp, ctypes.c_char_p)
+_sig("ccl_strip_group_rows", _c, _vp, _u32p, _u32p)
+_sig("ccl_strip_group_label", _c, _vp, _vp, _sz, _vp, _c, _vp)
+_sig("ccl_strip_group_launches", _c, _vp)
+_sig("ccl_strip_group_destroy", None, _vp)
 _sig("ccl_label_strips", _c, ctypes.POINTER(_c), _c, _u8p, _u32, _u32, _u32p, _c, ctypes.POINTER(ctypes.c_float))
 _sig("ccl_read_metrics", _c, _vp, _u32p, _u32p, _sz, ctypes.POINTER(ctypes.c_uint64), _u32p, _u32p, _u32p)
 _sig("ccl_gen_random", _c, _u8p, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
@@ -105,7 +112,9 @@ C_ABI_SYMBOLS = [
     "ccl_gen_random_device", "ccl_label_to_cclm", "ccl_write_label_map", "ccl_read_label_map", "ccl_io_last_error",
     "ccl_strip_local", "ccl_strip_seam_export", "ccl_strip_seam_resolve", "ccl_strip_final",
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
-    "ccl_launches_per_label", "ccl_label_strips", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
+    "ccl_launches_per_label", "ccl_label_strips", "ccl_strip_group_handle_bytes", "ccl_strip_group_create",
+    "ccl_strip_group_connect", "ccl_strip_group_rows", "ccl_strip_group_label", "ccl_strip_group_launches",
+    "ccl_strip_group_destroy", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
 ]
 
 _EINVAL, _ENOMEM, _ECUDA, _ENODEV = 1, 2, 3, 4
@@ -232,9 +241,11 @@ class Context:
             pass
 
 
+import atexit as _atexit
 import threading as _threading
 
 _tls = _threading.local()
+_all_ctxs: list = []  # every implicit context, released at interpreter exit
 
 
 def _ctx(device: int = 0) -> Context:
@@ -243,7 +254,15 @@ def _ctx(device: int = 0) -> Context:
         ctxs = _tls.ctxs = {}
     if device not in ctxs:
         ctxs[device] = Context(device)
+        _all_ctxs.append(ctxs[device])
     return ctxs[device]
+
+
+@_atexit.register
+def _release_contexts():
+    for c in _all_ctxs:
+        c.close()
+    _all_ctxs.clear()
 
 
 # ------------------------------------------------------------- the drop-in

@@ -144,7 +144,14 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
     std::memset(&a->tm_img, 0, sizeof(a->tm_img));
     std::memset(&a->tm_lab, 0, sizeof(a->tm_lab));
     const cclk::Geo& g = a->g;
-    EncodeFn enc = encode_fn();
+    // CCL_NO_TMA=1 (diagnostics only, e.g. compute-sanitizer initcheck, which
+    // does not see bulk-tensor stores as initialising writes): generic loads /
+    // stores instead of the TMA tile paths.  Same labels, slower.
+    static const bool no_tma = [] {
+        const char* v = std::getenv("CCL_NO_TMA");
+        return v && v[0] == '1';
+    }();
+    EncodeFn enc = no_tma ? nullptr : encode_fn();
     a->tma_load = enc && (reinterpret_cast<uintptr_t>(img) % 16 == 0) && (pitch % 16 == 0) &&
                   (frame_pitch % 16 == 0) && pitch < (uint64_t(1) << 40);
     a->tma_store = enc && (reinterpret_cast<uintptr_t>(labels) % 16 == 0) && (uint64_t(g.W) * 4 % 16 == 0);
@@ -693,117 +700,12 @@ const char* ccl_version(void) { return "ccl-b200 0.1 (sm_100a)"; }
 
 }  // extern "C"
 
-// ---------------------------------------------------------------------------
-// One image over several devices in one process (SURVEY §8b ccl_label_strips):
-// the strip protocol above with one host thread and one context per strip.
-// Phase 1 runs (a)(b)(c)(d) and the seam export on every strip; after all have
-// finished, every strip gathers the n seam exports with peer copies (NVLink
-// when the devices are peers; a plain device copy when a device is listed more
-// than once), resolves the seam forest redundantly and runs (e).
-ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, uint32_t w, uint32_t h,
-                            uint32_t* labels, int variant, float* kernel_ms) {
-    if (!devices || ndev <= 0 || !img || !labels) return fail(CCL_EINVAL, "null argument or no devices");
-    if (ccl_status s = check_dims(w, h)) return s;
-    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
-    const uint32_t th = uint32_t(cclk::tile_h()), tiles = (h + th - 1) / th, n = uint32_t(ndev);
-    if (n > tiles) return fail(CCL_EINVAL, "image has fewer tile rows than strips");
-    struct Strip {
-        int dev = 0;
-        uint32_t r0 = 0, h = 0;
-        ccl_ctx* ctx = nullptr;
-        uint8_t* d_img = nullptr;
-        uint32_t *d_lab = nullptr, *d_seam = nullptr, *d_all = nullptr, *d_scratch = nullptr;
-        void* d_work = nullptr;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        ccl_status st = CCL_OK;
-        std::string err;
-        float ms = 0.f;
-    };
-    std::vector<Strip> S(n);
-    for (uint32_t k = 0, acc = 0; k < n; ++k) {  // strips.split_rows: all but the last a multiple of th
-        const uint32_t t = tiles / n + (k < tiles % n ? 1u : 0u);
-        S[k].dev = devices[k];
-        S[k].r0 = acc;
-        S[k].h = k + 1 < n ? std::min(t * th, h - acc) : h - acc;
-        if (S[k].h == 0) return fail(CCL_EINVAL, "image has fewer tile rows than strips");
-        acc += S[k].h;
-    }
-    const size_t pitch = (size_t(w) + 15) / 16 * 16;
-    // run body(k) for every strip on its own thread; first failure wins
-    auto parallel = [&](auto&& body) -> ccl_status {
-        std::vector<std::thread> pool;
-        for (uint32_t k = 0; k < n; ++k)
-            pool.emplace_back([&, k] {
-                DeviceGuard dg(S[k].dev);
-                cudaSetDevice(S[k].dev);
-                S[k].st = body(S[k], k);
-                if (S[k].st != CCL_OK) S[k].err = ccl_last_error();
-            });
-        for (auto& t : pool) t.join();
-        for (auto& s : S)
-            if (s.st != CCL_OK) return fail(s.st, s.err);
-        return CCL_OK;
-    };
-    auto cleanup = [&] {
-        for (auto& s : S) {
-            DeviceGuard dg(s.dev);
-            cudaSetDevice(s.dev);
-            if (s.ctx) cudaStreamSynchronize(static_cast<cudaStream_t>(ccl_ctx_stream(s.ctx)));
-            cudaFree(s.d_img);
-            cudaFree(s.d_lab);
-            cudaFree(s.d_seam);
-            cudaFree(s.d_all);
-            cudaFree(s.d_scratch);
-            cudaFree(s.d_work);
-            if (s.e0) cudaEventDestroy(s.e0);
-            if (s.e1) cudaEventDestroy(s.e1);
-            if (s.ctx) ccl_ctx_destroy(s.ctx);
-        }
-    };
-    ccl_status st = parallel([&](Strip& s, uint32_t k) -> ccl_status {
-        if (ccl_status r = ccl_ctx_create(s.dev, &s.ctx)) return r;
-        cudaStream_t q = static_cast<cudaStream_t>(ccl_ctx_stream(s.ctx));
-        const size_t wb = ccl_work_bytes(w, s.h, 1);
-        CCL_CHECK(cudaMalloc(&s.d_img, pitch * s.h));
-        CCL_CHECK(cudaMalloc(&s.d_lab, size_t(w) * s.h * 4));
-        CCL_CHECK(cudaMalloc(&s.d_seam, size_t(4) * w * 4));
-        CCL_CHECK(cudaMalloc(&s.d_all, size_t(n) * 4 * w * 4));
-        CCL_CHECK(cudaMalloc(&s.d_scratch, ccl_strip_scratch_words(n, w) * 4));
-        CCL_CHECK(cudaMalloc(&s.d_work, wb));
-        CCL_CHECK(cudaMemsetAsync(s.d_work, 0, wb, q));
-        CCL_CHECK(cudaEventCreate(&s.e0));
-        CCL_CHECK(cudaEventCreate(&s.e1));
-        CCL_CHECK(cudaMemcpy2DAsync(s.d_img, pitch, img + size_t(s.r0) * w, w, w, s.h, cudaMemcpyHostToDevice, q));
-        CCL_CHECK(cudaEventRecord(s.e0, q));
-        if (ccl_status r = ccl_strip_local(s.ctx, s.d_img, pitch, w, s.h, s.r0, h, s.d_lab, s.d_work, variant, q))
-            return r;
-        if (ccl_status r = ccl_strip_seam_export(s.ctx, w, s.h, s.r0, h, k, s.d_lab, s.d_work, s.d_seam, q)) return r;
-        CCL_CHECK(cudaStreamSynchronize(q));
-        return CCL_OK;
-    });
-    if (st == CCL_OK)
-        st = parallel([&](Strip& s, uint32_t k) -> ccl_status {
-            cudaStream_t q = static_cast<cudaStream_t>(ccl_ctx_stream(s.ctx));
-            for (uint32_t j = 0; j < n; ++j)  // the all-gather: n peer reads of 16*W bytes
-                CCL_CHECK(cudaMemcpyPeerAsync(s.d_all + size_t(j) * 4 * w, s.dev, S[j].d_seam, S[j].dev,
-                                              size_t(4) * w * 4, q));
-            if (ccl_status r = ccl_strip_seam_resolve(s.ctx, s.d_all, n, k, w, s.h, s.r0, h, s.d_lab, s.d_work,
-                                                      s.d_scratch, q))
-                return r;
-            if (ccl_status r = ccl_strip_final(s.ctx, w, s.h, s.r0, h, s.d_lab, s.d_work, variant, q)) return r;
-            CCL_CHECK(cudaEventRecord(s.e1, q));
-            CCL_CHECK(cudaMemcpyAsync(labels + size_t(s.r0) * w, s.d_lab, size_t(w) * s.h * 4, cudaMemcpyDeviceToHost,
-                                      q));
-            CCL_CHECK(cudaStreamSynchronize(q));
-            CCL_CHECK(cudaEventElapsedTime(&s.ms, s.e0, s.e1));
-            return CCL_OK;
-        });
-    if (st == CCL_OK && kernel_ms) {
-        float m = 0.f;
-        for (auto& s : S) m = std::max(m, s.ms);
-        *kernel_ms = m;
-    }
-    const std::string err = st == CCL_OK ? std::string() : ccl_last_error();
-    cleanup();
-    return st == CCL_OK ? CCL_OK : fail(st, err);
+// ccl_label_strips (one image over several devices of this process) and the
+// multi-process strip groups live in ccl_strips.cu.
+
+namespace cclk {
+int set_error(int status, const char* msg) {
+    g_err = msg ? msg : "";
+    return status;
 }
+}  // namespace cclk

@@ -128,6 +128,8 @@ size_t work_bytes(uint32_t w, uint32_t h, uint32_t nframes);
 uint32_t* strip_area_ptr(uint32_t* work, const Geo& g);  // strip mode: [edge nodes 2W | edge roots 2W]
 uint32_t* forest_ptr(uint32_t* work, const Geo& g);      // compact global forest
 int tile_maxf();
+// records the thread-local message ccl_last_error() returns (ccl_capi.cu); returns status
+int set_error(int status, const char* msg);
 int tile_w();
 int tile_h();
 

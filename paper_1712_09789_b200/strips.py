@@ -5,8 +5,10 @@ Protocol (include/ccl_cuda.h, csrc/ccl_aux.cu):
                              GLOBAL raster space (x + (row0 + y) * W)
   2. ccl_strip_seam_export   4*W u32: strip roots of the top/bottom rows and
                              the first seam node carrying each root
-  3. all-gather              NCCL all_gather_into_tensor of every strip's 4*W
-                             words (the only cross-GPU traffic: 16*W bytes/GPU)
+  3. exchange               every strip's 4*W words stored into every rank's
+                             exchange area over NVLink + device epoch flags
+                             (library strip groups, StripLabeler); a device-
+                             local concatenation for virtual strips
   4. ccl_strip_seam_resolve  identical union-find over all seam nodes on every
                              rank, then each rank writes its seam roots' final
                              labels into its own forest
@@ -47,40 +49,63 @@ def exchange_seams(seam_local, world: int, group=None):
     return out.view((world,) + tuple(seam_local.shape))
 
 
-class StripLabeler:
-    """Labels this rank's strip; the seam exchange runs over torch.distributed."""
+def gather_handles(mine: bytes, world: int, group=None) -> bytes:
+    """All ranks' exchange-area handles concatenated in rank order (setup only;
+    any torch.distributed backend)."""
+    if world == 1:
+        return mine
+    import torch.distributed as dist
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    if any(len(h) != len(mine) for h in allh):
+        raise RuntimeError("strip group handles differ in size across ranks")
+    return b"".join(allh)
 
-    def __init__(self, ctx: Context, w: int, h: int, row0: int, full_h: int, rank: int, world: int, device,
-                 group=None):
-        import torch
-        self.ctx, self.w, self.h, self.row0, self.full_h = ctx, w, h, row0, full_h
-        self.rank, self.world, self.group = rank, world, group
-        self.seam = torch.empty(4 * w, dtype=torch.int32, device=device)
-        self.scratch = torch.empty(int(_lib.ccl_strip_scratch_words(world, w)), dtype=torch.int32, device=device)
-        self.work = torch.zeros(int(_lib.ccl_work_bytes(w, h, 1)), dtype=torch.uint8, device=device)
+
+class StripLabeler:
+    """This rank's strip of an N-GPU strip labeling (one process per GPU).
+
+    The seam exchange runs INSIDE the library (include/ccl_cuda.h strip
+    groups): each step stores this rank's 16*W-byte seam export into every
+    rank's exchange area over NVLink (areas shared with CUDA IPC handles) and
+    waits on device flags -- no host round trip, no torch collective in the
+    step.  torch.distributed is used once, at construction, to all-gather the
+    IPC handles (any backend; ``group`` selects the process group)."""
+
+    def __init__(self, ctx: Context, w: int, full_h: int, rank: int, world: int, group=None):
+        self.ctx, self.w, self.full_h, self.rank, self.world = ctx, w, full_h, rank, world
+        hb = int(_lib.ccl_strip_group_handle_bytes())
+        handle = ctypes.create_string_buffer(hb)
+        g = ctypes.c_void_p()
+        _check(_lib.ccl_strip_group_create(ctx.handle, rank, world, w, full_h, ctypes.byref(g), handle))
+        self._g = g
+        blob = ctypes.create_string_buffer(gather_handles(bytes(handle.raw), world, group), hb * world)
+        _check(_lib.ccl_strip_group_connect(g, blob))
+        r0, h = ctypes.c_uint32(), ctypes.c_uint32()
+        _check(_lib.ccl_strip_group_rows(g, ctypes.byref(r0), ctypes.byref(h)))
+        self.row0, self.h = int(r0.value), int(h.value)
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.ccl_strip_group_launches(self._g))
 
     def label(self, img, out, variant="c2fl", stream=None):
-        import torch
-        v = int(Variant.parse(variant))
-        s = _stream_ptr(stream)
-        c = self.ctx.handle
-        _check(_lib.ccl_strip_local(c, img.data_ptr(), img.stride(0), self.w, self.h, self.row0, self.full_h,
-                                    out.data_ptr(), self.work.data_ptr(), v, s))
-        _check(_lib.ccl_strip_seam_export(c, self.w, self.h, self.row0, self.full_h, self.rank, out.data_ptr(),
-                                          self.work.data_ptr(), self.seam.data_ptr(), s))
-        if stream is not None and not isinstance(stream, int):
-            with torch.cuda.stream(stream):
-                allseams = exchange_seams(self.seam, self.world, self.group)
-        else:
-            allseams = exchange_seams(self.seam, self.world, self.group)
-            if stream is not None:  # raw stream handle: keep the gather alive until it has run
-                torch.cuda.current_stream().synchronize()
-        _check(_lib.ccl_strip_seam_resolve(c, allseams.data_ptr(), self.world, self.rank, self.w, self.h, self.row0,
-                                           self.full_h, out.data_ptr(), self.work.data_ptr(), self.scratch.data_ptr(),
-                                           s))
-        _check(_lib.ccl_strip_final(c, self.w, self.h, self.row0, self.full_h, out.data_ptr(), self.work.data_ptr(),
-                                    v, s))
+        """img: (h, W) uint8 CUDA tensor holding rows [row0, row0+h); out: (h, W)
+        32-bit tensor, receives GLOBAL raster labels.  Asynchronous on stream."""
+        _check(_lib.ccl_strip_group_label(self._g, img.data_ptr(), img.stride(0), out.data_ptr(),
+                                          int(Variant.parse(variant)), _stream_ptr(stream)))
         return out
+
+    def close(self):
+        if getattr(self, "_g", None):
+            _lib.ccl_strip_group_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def label_strips_single_gpu(img, n_strips: int, variant="c2fl", stream=None, ctx: Context | None = None):

@@ -11,6 +11,13 @@ sys.path.insert(0, REPO)
 import oracle  # noqa: E402
 import paper_1712_09789_b200 as ccl  # noqa: E402
 
+if len(sys.argv) > 1 and sys.argv[1] == "small":  # full hazard listing (racecheck)
+    for name, img in [("random512", ccl.random_image(512, 512, 0.5, 0)),
+                      ("spiral256", ccl.pattern_image("spiral", 256, 256))]:
+        assert np.array_equal(ccl.label_image(img).label_map.labels, oracle.sequential_ccl(img)), name
+        print("ok", name, flush=True)
+    print("SANITIZE_RUN_DONE")
+    sys.exit(0)
 cases = [("random2048", ccl.random_image(2048, 2048, 0.5, 0)),
          ("spiral1024", ccl.pattern_image("spiral", 1024, 1024)),
          ("checker512", ccl.pattern_image("checkerboard", 512, 512)),

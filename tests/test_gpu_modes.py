@@ -103,13 +103,16 @@ def _strip_rank(rank, world, port, w, full_h, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         img = ccl.random_image(w, full_h, 0.58, 21)
-        row0, h = split_rows(full_h, world)[rank]
         dev = torch.device("cuda", 0)
+        lab = StripLabeler(ccl.Context(0), w, full_h, rank, world)
+        row0, h = lab.row0, lab.h
+        assert (row0, h) == split_rows(full_h, world)[rank]
         d_img = torch.from_numpy(np.ascontiguousarray(img[row0:row0 + h])).to(dev)
         out = torch.empty((h, w), dtype=torch.uint32, device=dev)
-        lab = StripLabeler(ccl.Context(0), w, h, row0, full_h, rank, world, dev)
-        lab.label(d_img, out)
-        torch.cuda.synchronize()
+        for _ in range(3):  # repeated steps: both export parities, epochs advance
+            out.fill_(7)
+            lab.label(d_img, out)
+            torch.cuda.synchronize()
         mine = out.cpu().view(torch.int32)
         hmax = max(hh for _, hh in split_rows(full_h, world))
         pad = torch.zeros((hmax, w), dtype=torch.int32)
@@ -126,8 +129,9 @@ def _strip_rank(rank, world, port, w, full_h, q):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_strip_labeler_multiprocess(ccl, world):
-    """StripLabeler (the bench's N>1 path) in `world` processes sharing one GPU;
-    the all-gather runs over gloo instead of NCCL (one GPU on the test box)."""
+    """StripLabeler (the bench's N>1 path) in `world` processes sharing one GPU:
+    library strip groups with CUDA IPC exchange areas and device flags (the
+    handles are all-gathered over gloo once)."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()

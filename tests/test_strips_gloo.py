@@ -2,8 +2,10 @@
 
 Each rank labels its strip, exports the 4*W seam words in exactly the layout
 the CUDA kernels produce (csrc/ccl_aux.cu: roots of the top/bottom rows, then
-the global seam-node rep of each), exchanges them with the product's
-``strips.exchange_seams`` over gloo, runs the seam union-find and applies the
+the global seam-node rep of each), exchanges them with ``strips.exchange_seams``
+over gloo (the all-gather the library's strip groups perform with NVLink peer
+stores: every rank ends with every strip's export in rank order), checks the
+product's setup step ``strips.gather_handles`` (IPC handles, rank order), runs the seam union-find and applies the
 remap.  The per-strip labeling and the seam arithmetic here are a test-only
 numpy restatement of the kernels; the GPU path itself is covered by
 tests/test_gpu_modes.py::test_virtual_strips.  The stitched result must be
@@ -83,11 +85,14 @@ def _worker(rank, world, port, w, full_h, q):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import oracle
-    from paper_1712_09789_b200.strips import exchange_seams
+    from paper_1712_09789_b200.strips import exchange_seams, gather_handles
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        # strip-group setup: every rank's 64-byte IPC handle, rank order
+        blob = gather_handles(bytes([rank + 1]) * 64, world)
+        assert blob == b"".join(bytes([k + 1]) * 64 for k in range(world)), "handle all-gather"
         img = oracle.random_image(w, full_h, 0.58, 12) if w != 96 else oracle.pattern_image("spiral", w, full_h)
         th = 32
         tiles = -(-full_h // th)
