@@ -99,6 +99,9 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
  * first kernel to the last (exchange included). */
 ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, uint32_t w, uint32_t h,
                             uint32_t* labels, int variant, float* kernel_ms);
+/* Frees the contexts and buffers ccl_label_strips keeps for repeated shapes
+ * (call before exit for a leak-free teardown; later calls re-create them). */
+void ccl_release_caches(void);
 
 /* ---- Strip groups: one image over N GPUs, one process (rank) per GPU ----
  * The seam exchange is inside the library and needs no host round trip per

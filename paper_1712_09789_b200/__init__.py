@@ -99,6 +99,7 @@ _sig("ccl_strip_group_rows", _c, _vp, _u32p, _u32p)
 _sig("ccl_strip_group_label", _c, _vp, _vp, _sz, _vp, _c, _vp)
 _sig("ccl_strip_group_launches", _c, _vp)
 _sig("ccl_strip_group_destroy", None, _vp)
+_sig("ccl_release_caches", None)
 _sig("ccl_label_strips", _c, ctypes.POINTER(_c), _c, _u8p, _u32, _u32, _u32p, _c, ctypes.POINTER(ctypes.c_float))
 _sig("ccl_read_metrics", _c, _vp, _u32p, _u32p, _sz, ctypes.POINTER(ctypes.c_uint64), _u32p, _u32p, _u32p)
 _sig("ccl_gen_random", _c, _u8p, _u32, _u32, ctypes.c_double, ctypes.c_uint64)
@@ -114,7 +115,7 @@ C_ABI_SYMBOLS = [
     "ccl_strip_scratch_words", "ccl_work_bytes", "ccl_compact_device", "ccl_compact_scratch_words", "ccl_tile_shape",
     "ccl_launches_per_label", "ccl_label_strips", "ccl_strip_group_handle_bytes", "ccl_strip_group_create",
     "ccl_strip_group_connect", "ccl_strip_group_rows", "ccl_strip_group_label", "ccl_strip_group_launches",
-    "ccl_strip_group_destroy", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
+    "ccl_strip_group_destroy", "ccl_release_caches", "ccl_metrics_build", "ccl_read_metrics", "ccl_gen_random", "ccl_gen_pattern", "ccl_last_error", "ccl_version",
 ]
 
 _EINVAL, _ENOMEM, _ECUDA, _ENODEV = 1, 2, 3, 4
@@ -260,6 +261,7 @@ def _ctx(device: int = 0) -> Context:
 
 @_atexit.register
 def _release_contexts():
+    _lib.ccl_release_caches()
     for c in _all_ctxs:
         c.close()
     _all_ctxs.clear()

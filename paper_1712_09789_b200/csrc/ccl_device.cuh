@@ -48,7 +48,9 @@ __device__ __forceinline__ uint32_t eq1_nibble(uint32_t v) {
     const uint32_t x = v ^ 0x01010101u;                 // zero bytes where v == 1
     uint32_t y = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;       // high bit set where low 7 bits != 0
     y = ~(y | x | 0x7F7F7F7Fu);                         // 0x80 exactly in the zero bytes of x
-    return ((y >> 7) * 0x10204080u) >> 28;              // gather bits 0,8,16,24 -> nibble
+    // gather bits 7,15,23,31 -> nibble: the partial products land on distinct
+    // bits (7,14,15,21,22,23 below the nibble), so no carry reaches bits 28-31
+    return (y * 0x00204081u) >> 28;
 }
 __device__ __forceinline__ uint32_t eq1_mask16(uint4 q) {
     return eq1_nibble(q.x) | (eq1_nibble(q.y) << 4) | (eq1_nibble(q.z) << 8) | (eq1_nibble(q.w) << 12);

@@ -345,6 +345,9 @@ __device__ __forceinline__ uint32_t tile_prefix(uint32_t cnt, uint32_t* CNT, uin
     return band + inc - rowtot + left;
 }
 
+// Index of the lowest set bit of x != 0 (FLO only; __ffs costs a BREV more on the XU pipe).
+__device__ __forceinline__ uint32_t lowbit(uint32_t x) { return 31u - __clz(x & (0u - x)); }
+
 // Id of the node holding bit b of a word with starts st and prefix pfx (a bit
 // before the word's first start belongs to the node continuing from the left).
 __device__ __forceinline__ uint32_t node_of(uint32_t pfx, uint32_t st, uint32_t b) {
@@ -995,15 +998,46 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
             const uint32_t os = (o & ~(o << 1)) & ~ocont;
             const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
+#if CCL_COARSE1
+            // ONE pass over this word's band runs, in node-id order (the part of
+            // the word before its first band start belongs to a run of the word on
+            // the left, whose lane owns that node): a run whose span holds an
+            // overlap links to the band-above run of its FIRST overlap; otherwise
+            // it is a root coded by its minimum pixel, the first top-row pixel,
+            // else its first column in the bottom row.  Overlap segments never
+            // cross run boundaries, so the lowest overlap bit of a span starts an
+            // overlap segment; every other segment start goes to the union list.
+            uint32_t firstm = 0u;
+            {
+                uint32_t rem = bs[k];
+                node_t* dst = P + pfx[k];
+                while (rem) {
+                    const uint32_t lo = rem & (0u - rem);  // this run's start bit
+                    rem ^= lo;
+                    const uint32_t span = (rem & (0u - rem)) - lo;  // [start, next start); to bit 31 for the last run
+                    const uint32_t ov = o & span, tp = tm[k] & span;
+                    uint32_t v;
+                    if (ov) {
+                        const uint32_t f = ov & (0u - ov);
+                        firstm |= f;
+                        v = node_of(upfx[k], ubs[k], 31u - __clz(f));
+                    } else {
+                        v = tp ? kRoot | (rowpos0 + 31u - __clz(tp & (0u - tp))) : kRoot | (rowpos1 + 31u - __clz(lo));
+                    }
+                    *dst++ = node_t(v);
+                }
+            }
+            const bool last_has_top = bs[k] && (tm[k] >> (31u - __clz(bs[k])));
+#else
             // the part of the word before its first band start belongs to a band
             // run of the word on the left (that lane owns the node)
-            const uint32_t contp = bs[k] ? (1u << (__ffs(bs[k]) - 1)) - 1u : 0xFFFFFFFFu;
+            const uint32_t contp = bs[k] ? (1u << (lowbit(bs[k]))) - 1u : 0xFFFFFFFFu;
             const uint32_t firstm = seg_first(o, bs[k]) & ~contp;   // first overlap of each band run
             const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
             {   // a band run without a top-row pixel: a root coded by its first column
                 uint32_t tt = bs[k] & ~seg_back(tfirst, bs[k]);
                 while (tt) {
-                    const uint32_t a = __ffs(tt) - 1;
+                    const uint32_t a = lowbit(tt);
                     tt &= tt - 1;
                     P[node_of(pfx[k], bs[k], a)] = node_t(kRoot | (rowpos1 + a));
                 }
@@ -1014,35 +1048,35 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 // its first top-row pixel
                 uint32_t tt = tfirst, ff = firstm;
                 while (tt) {
-                    const uint32_t f = __ffs(tt) - 1;
+                    const uint32_t f = lowbit(tt);
                     tt &= tt - 1;
                     uint32_t v = kRoot | (rowpos0 + f);
                     // lowest overlap before the next run's first top pixel (an empty
                     // mask's isolated low bit - 1 wraps to "infinity")
                     if ((ff & (0u - ff)) - 1u < (tt & (0u - tt)) - 1u) {
-                        v = node_of(upfx[k], ubs[k], __ffs(ff) - 1);
+                        v = node_of(upfx[k], ubs[k], lowbit(ff));
                         ff &= ff - 1;
                     }
                     P[node_of(pfx[k], bs[k], f)] = node_t(v);
                 }
             }
-            if (bs[k] && (((tm[k] | um[k]) >> 31) & 1u)) {
-                // the last band run reaches the word's end: with no top-row pixel
-                // here, its top-row pixel may lie in a later word
-                const uint32_t a = 31u - __clz(bs[k]);
-                if (!(tfirst & (0xFFFFFFFFu << a))) {
-                    for (int w = wc + 1; w < WPR; ++w) {
-                        const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
-                        const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
-                        const uint32_t below = bw ? (1u << (__ffs(bw) - 1)) - 1u : 0xFFFFFFFFu;
-                        const uint32_t cont = (tw | uw) & below;  // the part continuing from the left
-                        const uint32_t tc = tw & cont;
-                        if (tc) {
-                            P[pfx[k] + __popc(bs[k]) - 1] = node_t(kRoot | (uint32_t(r0 * C::TW + 32 * w) + __ffs(tc) - 1));
-                            break;
-                        }
-                        if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
+            const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
+#endif
+            if (bs[k] && (((tm[k] | um[k]) >> 31) & 1u) && !last_has_top) {
+                // the last band run reaches the word's end with no top-row pixel
+                // here: its top-row pixel may lie in a later word
+                for (int w = wc + 1; w < WPR; ++w) {
+                    const uint32_t tw = M[r0 * WPR + w], uw = M[r1 * WPR + w];
+                    const uint32_t bw = band_starts(tw, uw, M[r0 * WPR + w - 1], M[r1 * WPR + w - 1]);
+                    const uint32_t below = (bw & (0u - bw)) - 1u;  // bits before the first start (all if none)
+                    const uint32_t cont = (tw | uw) & below;       // the part continuing from the left
+                    const uint32_t tc = tw & cont;
+                    if (tc) {
+                        P[pfx[k] + __popc(bs[k]) - 1] =
+                            node_t(kRoot | (uint32_t(r0 * C::TW + 32 * w) + 31u - __clz(tc & (0u - tc))));
+                        break;
                     }
+                    if (bw || cont != 0xFFFFFFFFu) break;  // the run ends in this word
                 }
             }
             U[k] = os & ~firstm;  // remaining overlaps
@@ -1067,7 +1101,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 #pragma unroll
                 for (int k = 0; k < WPL; ++k) {
                     while (U[k]) {
-                        const uint32_t b = __ffs(U[k]) - 1;
+                        const uint32_t b = lowbit(U[k]);
                         U[k] &= U[k] - 1;
                         *dst++ = node_of(pfx[k], bs[k], b) | (node_of(upfx[k], ubs[k], b) << 16);
                     }
@@ -1098,7 +1132,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             while (U[k]) {  // pairs that did not fit in the list
-                const uint32_t b = __ffs(U[k]) - 1;
+                const uint32_t b = lowbit(U[k]);
                 U[k] &= U[k] - 1;
                 nunion_pos(P, node_of(pfx[k], bs[k], b), node_of(upfx[k], ubs[k], b), mc);
             }

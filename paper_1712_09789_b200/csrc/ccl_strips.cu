@@ -15,7 +15,7 @@
 //                                 pointer in-process); the last CTA to finish raises
 //                                 flag `rank` = epoch in every area (release, system scope)
 //   4. k_strip_wait               one thread per peer spins on its LOCAL flag until it
-//                                 reaches this epoch (acquire, system scope)
+//                                 reaches this epoch or a later one (acquire, system scope)
 //   5. ccl_strip_seam_resolve     the same union-find over all N exports on every rank
 //                                 (no broadcast: the local area already holds them)
 //   6. ccl_strip_final            kernels (d2)+(e)
@@ -108,12 +108,33 @@ __global__ void k_strip_wait(const uint32_t* flags, uint32_t n_ranks, uint32_t r
     const uint32_t k = threadIdx.x;
     if (k >= n_ranks || k == rank) return;
     const uint64_t t0 = globaltimer();
-    while (ld_acquire_sys(flags + k) != epoch) {
+    // >=, not ==: a fast peer may already have published a LATER epoch here
+    // (it only needs this rank's current export, which is still in its parity
+    // slot: the peer cannot run two steps ahead, see the header)
+    while (int32_t(ld_acquire_sys(flags + k) - epoch) < 0) {
         if (globaltimer() - t0 > kWaitTimeoutNs) __trap();  // a peer never arrived: fail loudly
         __nanosleep(64);
     }
 }
 
+}  // namespace
+
+namespace {
+// ccl_label_strips' per-shape resources.  Never destroyed by a static
+// destructor (CUDA must not be called after the runtime's own teardown at
+// exit); ccl_release_caches() frees them explicitly.
+std::mutex& strips_mu() {
+    static std::mutex mu;
+    return mu;
+}
+using StripsKey = std::tuple<std::vector<int>, uint32_t, uint32_t>;
+struct CacheBase {
+    virtual ~CacheBase() = default;
+};
+std::map<StripsKey, std::unique_ptr<CacheBase>>& strips_cache_base() {
+    static auto* m = new std::map<StripsKey, std::unique_ptr<CacheBase>>();
+    return *m;
+}
 }  // namespace
 
 struct ccl_strip_group {
@@ -336,9 +357,9 @@ ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, ui
         uint32_t* d_lab = nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr, mid = nullptr;
     };
-    struct Setup {
+    struct Setup : CacheBase {
         std::vector<Strip> s;
-        ~Setup() {
+        ~Setup() override {
             for (auto& x : s) {
                 DevScope ds(x.dev);
                 if (x.g) group_free(x.g);
@@ -350,13 +371,9 @@ ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, ui
             }
         }
     };
-    using Key = std::tuple<std::vector<int>, uint32_t, uint32_t>;
-    static std::mutex mu;
-    // never destroyed: its CUDA resources must not be released after the
-    // runtime's own teardown at process exit
-    static auto& cache = *new std::map<Key, std::unique_ptr<Setup>>();
-    std::lock_guard<std::mutex> lk(mu);
-    const Key key{std::vector<int>(devices, devices + n), w, h};
+    std::lock_guard<std::mutex> lk(strips_mu());
+    auto& cache = strips_cache_base();
+    const StripsKey key{std::vector<int>(devices, devices + n), w, h};
     auto it = cache.find(key);
     if (it == cache.end()) {
         if (cache.size() >= 2) cache.clear();  // bound the device memory kept alive
@@ -395,7 +412,7 @@ ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, ui
         }
         it = cache.emplace(key, std::move(su)).first;
     }
-    std::vector<Strip>& S = it->second->s;
+    std::vector<Strip>& S = static_cast<Setup*>(it->second.get())->s;
     const size_t pitch = (size_t(w) + 15) / 16 * 16;
     for (uint32_t k = 0; k < n; ++k) {  // phase 1 everywhere
         Strip& s = S[k];
@@ -429,6 +446,11 @@ ccl_status ccl_label_strips(const int* devices, int ndev, const uint8_t* img, ui
     }
     if (kernel_ms) *kernel_ms = worst;
     return CCL_OK;
+}
+
+void ccl_release_caches(void) {
+    std::lock_guard<std::mutex> lk(strips_mu());
+    strips_cache_base().clear();
 }
 
 }  // extern "C"
