@@ -94,6 +94,10 @@ struct ccl_ctx {
     uint32_t m_tx = 0, m_ty = 0, m_frames = 0;
     ccl_timing last{};
     bool last_split = false;
+    // pipelined batches: second stream for kernels (d2)+(e) of chunk j while
+    // kernels (a)+(d) of chunk j+1 run on the call's stream
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t pev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -304,6 +308,9 @@ void ccl_ctx_destroy(ccl_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
+    for (auto& e : c->pev)
+        if (e) cudaEventDestroy(e);
     if (c->d_img) cudaFree(c->d_img);
     if (c->d_lab) cudaFree(c->d_lab);
     if (c->h_img) cudaFreeHost(c->h_img);
@@ -370,6 +377,13 @@ ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch
     return CCL_OK;
 }
 
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+}  // namespace
+
 ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pitch, size_t frame_pitch, uint32_t n,
                            uint32_t w, uint32_t h, uint32_t* d_labels, int variant, void* stream) {
     if (!ctx || !d_frames || !d_labels) return fail(CCL_EINVAL, "null argument");
@@ -377,14 +391,61 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     if (n > 65535) return fail(CCL_EINVAL, "at most 65535 frames per batch call");
     if (ccl_status s = check_dims(w, h)) return s;
     if (img_pitch < w || frame_pitch < img_pitch * h) return fail(CCL_EINVAL, "bad pitch");
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
     DeviceGuard dg(ctx->device);
-    cclk::LaunchArgs a{};
-    if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ccl_status s = prepare(&a, d_frames, img_pitch, frame_pitch, n, d_labels, variant, st)) return s;
-    if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, n), st)) return s;
-    a.work = static_cast<uint32_t*>(ctx->d_work);
-    return run_pipeline(ctx, a, true);
+    // Frames are independent, so a big batch is labeled as a PIPELINE of
+    // chunks over two streams: kernels (a)+(d) of chunk j+1 (issue-bound) run
+    // while kernels (d2)+(e) of chunk j (HBM-bound: the label stores) drain,
+    // with the persistent grids capped so both fit on every SM.  Each chunk
+    // has its own work region, so the chunks share nothing.
+    const uint32_t tiles_per_frame = ((w + cclk::tile_w() - 1) / cclk::tile_w()) * ((h + cclk::tile_h() - 1) / cclk::tile_h());
+    const uint32_t min_chunk_tiles = uint32_t(env_int("CCL_PIPE_TILES", 16384));
+    const uint32_t chunk = std::max(1u, (min_chunk_tiles + tiles_per_frame - 1) / tiles_per_frame);
+    const bool pipe = env_int("CCL_PIPE", 1) != 0 && n >= 3 * chunk && !CCL_METRICS && !CCL_FUSE_SEAMS;
+    if (!pipe) {
+        cclk::LaunchArgs a{};
+        if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
+        if (ccl_status s = prepare(&a, d_frames, img_pitch, frame_pitch, n, d_labels, variant, st)) return s;
+        if (ccl_status s = ensure_work(ctx, cclk::work_bytes(w, h, n), st)) return s;
+        a.work = static_cast<uint32_t*>(ctx->d_work);
+        return run_pipeline(ctx, a, true);
+    }
+    const uint32_t nchunks = (n + chunk - 1) / chunk;
+    const size_t wb = (cclk::work_bytes(w, h, chunk) + 255) / 256 * 256;  // per chunk
+    if (ccl_status s = ensure_work(ctx, wb * nchunks, st)) return s;
+    if (!ctx->stream2) {
+        CCL_CHECK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+        for (auto& e : ctx->pev) CCL_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t s2 = ctx->stream2;
+    ctx->last_split = false;
+    CCL_CHECK(cudaEventRecord(ctx->ev[0], st));
+    CCL_CHECK(cudaStreamWaitEvent(s2, ctx->ev[0], 0));  // inputs / previous work on the caller's stream
+    const int acap = env_int("CCL_PIPE_A", 7), ecap = env_int("CCL_PIPE_E", 3);  // tuned: scripts/batch_sweep.py
+    for (uint32_t j = 0; j < nchunks; ++j) {
+        const uint32_t f0 = j * chunk, nj = std::min(chunk, n - f0);
+        cclk::LaunchArgs a{};
+        if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;
+        if (ccl_status s = prepare(&a, d_frames + size_t(f0) * frame_pitch, img_pitch, frame_pitch, nj,
+                                   d_labels + size_t(f0) * w * h, variant, st))
+            return s;
+        a.work = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ctx->d_work) + wb * j);
+        a.a_cap_per_sm = acap;
+        a.e_cap_per_sm = ecap;
+        a.g.epoch = next_epoch();
+        CCL_CHECK(cclk::launch_local(a));
+        CCL_CHECK(cclk::launch_seams(a));
+        CCL_CHECK(cudaEventRecord(ctx->pev[j & 1], st));
+        CCL_CHECK(cudaStreamWaitEvent(s2, ctx->pev[j & 1], 0));
+        a.stream = s2;
+        a.no_pdl_first = true;
+        CCL_CHECK(cclk::launch_final(a));
+    }
+    CCL_CHECK(cudaEventRecord(ctx->pev[0], s2));
+    CCL_CHECK(cudaStreamWaitEvent(st, ctx->pev[0], 0));  // the caller's stream sees every label
+    CCL_CHECK(cudaEventRecord(ctx->ev[3], st));
+    return CCL_OK;
 }
 
 ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels, int variant,

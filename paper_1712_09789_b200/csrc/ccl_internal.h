@@ -40,9 +40,6 @@
 #ifndef CCL_SEAM_K
 #define CCL_SEAM_K 4  // kernel (d): 32-pair seam chunks per warp (unions compacted over the warp)
 #endif
-#ifndef CCL_COARSE1
-#define CCL_COARSE1 1  // band kernel (a): one pass over the band runs of a word (first-overlap link or root code)
-#endif
 #ifndef CCL_BJUMP
 #define CCL_BJUMP 1  // band kernel (a): pointer-jumping rounds before the unions
 #endif
@@ -111,6 +108,12 @@ struct LaunchArgs {
     uint32_t* labels;
     uint32_t* work;         // per-tile masks / run table / seam-root list (work_bytes)
     cudaStream_t stream;
+    // pipelined batches (ccl_label_batch): persistent grids capped at this many
+    // CTAs per SM (0 = full occupancy) so kernel (a) of one chunk and kernel (e)
+    // of the previous one share the SMs; the first launch of a group follows a
+    // cross-stream event, so it must not be a programmatic dependent launch
+    int a_cap_per_sm, e_cap_per_sm;
+    bool no_pdl_first;
 };
 
 cudaError_t launch_local(const LaunchArgs& a);

@@ -998,37 +998,6 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
             const uint32_t os = (o & ~(o << 1)) & ~ocont;
             const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
-#if CCL_COARSE1
-            // ONE pass over this word's band runs, in node-id order (the part of
-            // the word before its first band start belongs to a run of the word on
-            // the left, whose lane owns that node): a run whose span holds an
-            // overlap links to the band-above run of its FIRST overlap; otherwise
-            // it is a root coded by its minimum pixel, the first top-row pixel,
-            // else its first column in the bottom row.  Overlap segments never
-            // cross run boundaries, so the lowest overlap bit of a span starts an
-            // overlap segment; every other segment start goes to the union list.
-            uint32_t firstm = 0u;
-            {
-                uint32_t rem = bs[k];
-                node_t* dst = P + pfx[k];
-                while (rem) {
-                    const uint32_t lo = rem & (0u - rem);  // this run's start bit
-                    rem ^= lo;
-                    const uint32_t span = (rem & (0u - rem)) - lo;  // [start, next start); to bit 31 for the last run
-                    const uint32_t ov = o & span, tp = tm[k] & span;
-                    uint32_t v;
-                    if (ov) {
-                        const uint32_t f = ov & (0u - ov);
-                        firstm |= f;
-                        v = node_of(upfx[k], ubs[k], 31u - __clz(f));
-                    } else {
-                        v = tp ? kRoot | (rowpos0 + 31u - __clz(tp & (0u - tp))) : kRoot | (rowpos1 + 31u - __clz(lo));
-                    }
-                    *dst++ = node_t(v);
-                }
-            }
-            const bool last_has_top = bs[k] && (tm[k] >> (31u - __clz(bs[k])));
-#else
             // the part of the word before its first band start belongs to a band
             // run of the word on the left (that lane owns the node)
             const uint32_t contp = bs[k] ? (1u << (lowbit(bs[k]))) - 1u : 0xFFFFFFFFu;
@@ -1061,7 +1030,6 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
-#endif
             if (bs[k] && (((tm[k] | um[k]) >> 31) & 1u) && !last_has_top) {
                 // the last band run reaches the word's end with no top-row pixel
                 // here: its top-row pixel may lie in a later word
@@ -1590,13 +1558,13 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
 // (kernel, device, block, smem) -- each template instantiation has its own
 // entry -- under a mutex (strip workers call this from several host threads).
 template <class K>
-static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles) {
+static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles, int cap_per_sm = 0) {
     static std::mutex mu;
-    static std::map<std::tuple<const void*, int, int, int>, int> cache;
+    static std::map<std::tuple<const void*, int, int, int>, std::pair<int, int>> cache;  // {CTAs/SM, SMs}
     int dev = 0;
     cudaGetDevice(&dev);
     const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, threads, smem);
-    int per;
+    std::pair<int, int> occ;
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
@@ -1604,10 +1572,11 @@ static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles
             int n = 0, sms = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            it = cache.emplace(key, (n > 0 ? n : 1) * (sms > 0 ? sms : 1)).first;
+            it = cache.emplace(key, std::make_pair(n > 0 ? n : 1, sms > 0 ? sms : 1)).first;
         }
-        per = it->second;
+        occ = it->second;
     }
+    const int per = (cap_per_sm > 0 && cap_per_sm < occ.first ? cap_per_sm : occ.first) * occ.second;
     return unsigned(per < int(ntiles) ? per : int(ntiles));
 }
 
@@ -1674,7 +1643,8 @@ static cudaError_t launch_local_band(const LaunchArgs& a) {
         auto k = k_local_band<C, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt), nt)), C::NT, A::SMEM, a.stream, false,
+        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt, a.a_cap_per_sm), nt)), C::NT, A::SMEM,
+                      a.stream, false,
                       a.tm_img, a.img, a.work, a.g, nt);
     } else {
         auto k = k_local_band<C, false>;
@@ -1701,14 +1671,14 @@ static cudaError_t launch_final_v(const LaunchArgs& a) {
     using E = ELayout<C, RUNS, BAND>;
     const uint32_t nt = tile_count(a);
     constexpr int NTH = C::NT;
-    cudaError_t e = launch_pdl(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream,
-                               a.work, a.g, nt);
+    cudaError_t e = launch_ex(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream,
+                              !a.no_pdl_first, a.work, a.g, nt);
     if (e != cudaSuccess) return e;
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_pdl(k, dim3(persistent_grid(k, NTH, E::SMEM, nt)), NTH, E::SMEM, a.stream,
+        e = launch_pdl(k, dim3(persistent_grid(k, NTH, E::SMEM, nt, a.e_cap_per_sm)), NTH, E::SMEM, a.stream,
                        a.tm_lab, a.labels, const_cast<const uint32_t*>(a.work), a.g, nt);
     } else {
         auto k = k_final<C, RUNS, false, BAND>;

@@ -266,3 +266,21 @@ def test_label_host_async_two_contexts(ccl, oracle_mod):
         ccl._check(ccl._lib.ccl_ctx_sync(c.handle))
     for k in (len(imgs) - 2, len(imgs) - 1):
         assert np.array_equal(hout[k].numpy().view(np.uint32), oracle_mod.sequential_ccl(imgs[k])), k
+
+
+@pytest.mark.parametrize("pipe_tiles", ["50", "8192"])
+def test_batch_pipelined_chunks(ccl, oracle_mod, monkeypatch, pipe_tiles):
+    """ccl_label_batch as a two-stream pipeline of frame chunks (kernels (a)+(d)
+    of chunk j+1 beside (d2)+(e) of chunk j): small chunks forced through
+    CCL_PIPE_TILES, mixed content, ragged last chunk; every frame bit-exact."""
+    import torch
+    monkeypatch.setenv("CCL_PIPE_TILES", pipe_tiles)
+    w, h, n = 500, 300, 41
+    frames = np.stack([ccl.random_image(w, h, 0.3 + 0.01 * s, s) for s in range(n)])
+    frames[7] = ccl.pattern_image("spiral", w, h)
+    frames[8] = 1
+    frames[9] = 0
+    frames[10] = ccl.pattern_image("checkerboard", w, h)
+    got = ccl.label_batch_device(torch.from_numpy(frames).cuda()).cpu().numpy()
+    for f in range(n):
+        assert np.array_equal(got[f], oracle_mod.sequential_ccl(frames[f])), f
