@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -822,10 +823,11 @@ __device__ __forceinline__ void seam_chunk(const Forest& fst, const uint32_t* ra
     if (act) fst.unite(a, b, mc);
 }
 
+// Kernel (a) on band runs: CTA `cta` of `ncta` labels tiles cta, cta + ncta, ...
+// (the body of the persistent kernel below).
 template <class C, bool TMA>
-__global__ void __launch_bounds__(C::NT, CCL_BMINB)
-    k_local_band(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img, uint32_t* work, Geo g,
-                 uint32_t ntiles) {
+__device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const uint8_t* img, uint32_t* work,
+                                                 const Geo& g, uint32_t ntiles, uint32_t cta, uint32_t ncta) {
     static_assert(C::RPL == 2, "lane = 2-row band");
     using A = ALayout<C, true, true>;
     constexpr int WPL = C::WPL, WPR = C::WPR;
@@ -852,19 +854,19 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 
     auto issue_at = [&](const TileId& q) {
         mbar_expect_tx(bar, C::PX);
-        tma_load_3d_hint(IMG, &tm_img, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar, policy_evict_first());
+        tma_load_3d_hint(IMG, tmap, int(q.tx * C::TW), int(q.ty * C::TH), int(q.fz), bar, policy_evict_first());
     };
     if (TMA && tid == 0) {
-        prefetch_tmap(&tm_img);
+        prefetch_tmap(tmap);
         mbar_init(bar, 1);
-        if (blockIdx.x < ntiles) issue_at(tile_of(blockIdx.x, g));
+        if (cta < ntiles) issue_at(tile_of(cta, g));
     }
 
     uint32_t it = 0;
     CCL_PH_INIT();
     Ctr mc;  // instrumented builds: this thread's find steps / CAS attempts of the current tile
-    TileWalk walk(blockIdx.x, gridDim.x, g);
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, walk.advance()) {
+    TileWalk walk(cta, ncta, g);
+    for (uint32_t t = cta; t < ntiles; t += ncta, ++it, walk.advance()) {
         const TileId ti = walk.cur;
         const uint32_t tx = ti.tx, ty = ti.ty;
         const uint32_t x0 = tx * C::TW, y0 = ty * C::TH;
@@ -907,7 +909,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
         }
         __syncthreads();
         CCL_PH(9);
-        if (TMA && !A::OVL && tid == 0 && t + gridDim.x < ntiles) {
+        if (TMA && !A::OVL && tid == 0 && t + ncta < ntiles) {
             TileWalk nx = walk;
             nx.advance();
             issue_at(nx.cur);
@@ -1223,7 +1225,7 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
             __syncthreads();
             if (tid == 0) {
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                if (t + gridDim.x < ntiles) {
+                if (t + ncta < ntiles) {
                     TileWalk nx = walk;
                     nx.advance();
                     issue_at(nx.cur);
@@ -1234,6 +1236,13 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     CCL_PH_DONE();
+}
+
+template <class C, bool TMA>
+__global__ void __launch_bounds__(C::NT, CCL_BMINB)
+    k_local_band(const __grid_constant__ CUtensorMap tm_img, const uint8_t* img, uint32_t* work, Geo g,
+                 uint32_t ntiles) {
+    local_band_tiles<C, TMA>(&tm_img, img, work, g, ntiles, blockIdx.x, gridDim.x);
     pdl_trigger();
 }
 
@@ -1242,17 +1251,15 @@ __global__ void __launch_bounds__(C::NT, CCL_BMINB)
 // tile seam (coalesced record loads); a pair whose predecessor along the seam
 // is also foreground on both sides joins the same two local components and is
 // skipped (one union per overlapping run).  Global atomicMin union-find in L.
+// One warp's share of kernel (d): K consecutive 32-pair chunks starting at
+// chunk gw * K of frame fz; `list` = this warp's 32 K union slots (smem).
 template <class C>
-__global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t ntiles) {
+__device__ __forceinline__ void seams_warp(uint32_t* work, const Geo& g, uint32_t ntiles, uint32_t gw, uint32_t fz,
+                                           uint2* list) {
     constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
     constexpr int K = CCL_SEAM_K;                          // chunks per warp
-    __shared__ uint2 list[8][32 * K];                      // this warp's unions
-    const uint32_t fz = blockIdx.y;
     const Forest fst = forest_of<C>(work, ntiles);
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    pdl_wait();
-    pdl_trigger();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     Ctr mc;
     const uint32_t nh = (g.nty - 1) * g.ntx * HC;
     const uint32_t nv = (g.ntx - 1) * g.nty * VC;
@@ -1301,15 +1308,24 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
         act = act && (__ffs(same) - 1 == lane);
 #endif
         const uint32_t bal = __ballot_sync(0xffffffffu, act);
-        if (act) list[wib][n + __popc(bal & ((1u << lane) - 1u))] = make_uint2(va[k], vb[k]);
+        if (act) list[n + __popc(bal & ((1u << lane) - 1u))] = make_uint2(va[k], vb[k]);
         n += __popc(bal);
     }
     __syncwarp();
     for (uint32_t j = lane; j < n; j += 32) {
-        const uint2 pr = list[wib][j];
+        const uint2 pr = list[j];
         fst.unite(pr.x, pr.y, mc);
     }
+    __syncwarp();  // the list is reused by this warp's next share (fused kernel)
     metrics_phase(g, 0, mc);
+}
+
+template <class C>
+__global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t ntiles) {
+    __shared__ uint2 list[8][32 * CCL_SEAM_K];  // each warp's unions
+    pdl_wait();
+    pdl_trigger();
+    seams_warp<C>(work, g, ntiles, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, blockIdx.y, list[threadIdx.x >> 5]);
 }
 
 // ------------------------------------------------------------------ kernel (d2)
@@ -1317,18 +1333,55 @@ __global__ void __launch_bounds__(256) k_seams(uint32_t* work, Geo g, uint32_t n
 // final label of each tile's seam-touching roots, written over the tile's
 // root list, so kernel (e) needs no forest walks.  One warp per tile.
 template <class C>
-__global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t ntiles) {
-    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void resolve_tile(uint32_t* work, const Geo& g, uint32_t ntiles, uint32_t t) {
     const int lane = threadIdx.x & 31;
-    pdl_wait();
-    pdl_trigger();
-    if (t >= ntiles) return;
     uint32_t* wt = work_tile<C>(work, t);
     const uint32_t nf = wt[C::W_HEAD];
     const Forest fst = forest_of<C>(work, ntiles);
     Ctr mc;
-    for (uint32_t k = lane; k < nf; k += 32) wt[C::W_LIST + k] = fst.find_compress(t * uint32_t(C::MAXF) + k, mc).y;
+    // up to R roots of this lane climb at once (all first loads in flight
+    // together, then lockstep hops): ~1-2 dependent L2 round trips per group
+    // of 32 R roots instead of one chain per root
+    constexpr int R = 4;
+    const uint32_t base = t * uint32_t(C::MAXF);
+    for (uint32_t k0 = 0; k0 < nf; k0 += 32u * R) {
+        uint32_t cur[R];
+        uint2 v[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            cur[i] = base + k0 + lane + 32u * i;
+            if (k0 + lane + 32u * i < nf) v[i] = fst.node(cur[i]);
+        }
+        for (;;) {
+            bool more = false;
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (k0 + lane + 32u * i < nf && v[i].x != cur[i]) {
+                    mc.step();
+                    cur[i] = v[i].x;
+                    v[i] = fst.node(cur[i]);
+                    more = true;
+                }
+            if (!more) break;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const uint32_t k = k0 + lane + 32u * i;
+            if (k < nf) {
+                if (cur[i] != base + k) fst.f[2 * size_t(base + k)] = cur[i];  // path compression
+                wt[C::W_LIST + k] = v[i].y;
+            }
+        }
+    }
     metrics_phase(g, 2, mc);
+}
+
+template <class C>
+__global__ void __launch_bounds__(256, 8) k_resolve(uint32_t* work, Geo g, uint32_t ntiles) {
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    pdl_wait();
+    pdl_trigger();
+    if (t < ntiles) resolve_tile<C>(work, g, ntiles, t);
 }
 
 // ------------------------------------------------------------------ kernel (e)
@@ -1338,8 +1391,8 @@ __global__ void __launch_bounds__(256) k_resolve(uint32_t* work, Geo g, uint32_t
 // swizzled staging tile and writes it with one TMA store: every label is
 // written exactly once and the image is never re-read.
 template <class C, bool RUNS, bool TMA_ST, bool BAND>
-__global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
-                                                    const uint32_t* work, Geo g, uint32_t ntiles) {
+__device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L, const uint32_t* work, const Geo& g,
+                                            uint32_t ntiles, uint32_t cta, uint32_t ncta) {
     using E = ELayout<C, RUNS, BAND>;
     uint8_t* smem = aligned_smem();
     uint64_t* b1 = reinterpret_cast<uint64_t*>(smem + E::BAR_OFF);
@@ -1347,7 +1400,7 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane;
-    const uint32_t G = gridDim.x;
+    const uint32_t G = ncta;
     auto s1buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S1_OFF + j * E::S1); };
     auto s2buf = [&](uint32_t j) { return reinterpret_cast<uint32_t*>(smem + E::S2_OFF + j * E::S2); };
     auto s1 = [&](uint32_t t, uint32_t j) {
@@ -1362,11 +1415,11 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         if (lb) bulk_load(s2buf(j), wt + C::W_LIST, lb, &b2[j]);
         if (tb) bulk_load(s2buf(j) + C::MAXF, wt + C::W_TBL, tb, &b2[j]);
     };
-    if (tid == 0 && TMA_ST) prefetch_tmap(&tm_lab);
+    if (tid == 0 && TMA_ST) prefetch_tmap(tmap);
     if (tid == 0) {
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
         for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
-        const uint32_t t0 = blockIdx.x;
+        const uint32_t t0 = cta;
         // heads / masks come from kernel (a), complete before (d2) let this grid
         // launch; only the seam labels of (d2) need the dependency wait.  Every
         // other thread reads global data only through thread 0's copies.
@@ -1382,8 +1435,8 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
 
     const int sw = lane & 7;
     uint32_t it = 0;
-    TileWalk walk(blockIdx.x, G, g);
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it, walk.advance()) {
+    TileWalk walk(cta, G, g);
+    for (uint32_t t = cta; t < ntiles; t += G, ++it, walk.advance()) {
         const uint32_t j1 = it % 3, j2 = it & 1u;
         if (tid == 0) {
             if (t + 2 * G < ntiles) s1(t + 2 * G, (it + 2) % 3);
@@ -1471,7 +1524,7 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
                 if (lane == 0) {
                     for (int kk = 0; kk < 2; ++kk) {
                         uint8_t* sk = smem + E::STG_OFF + (warp * 2 + kk) * 4096;
-                        tma_store_3d_hint(&tm_lab, int(x0 + wc * 32), int(y0 + 64 * wy + 32 * kk), int(ti.fz), sk,
+                        tma_store_3d_hint(tmap, int(x0 + wc * 32), int(y0 + 64 * wy + 32 * kk), int(ti.fz), sk,
                                           policy_evict_first());
                     }
                 }
@@ -1539,10 +1592,10 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
                 __syncwarp();
                 if (lane == 0) {
                     if (CCL_HINTS)
-                        tma_store_3d_hint(&tm_lab, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg,
+                        tma_store_3d_hint(tmap, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg,
                                           policy_evict_first());  // OOB clipped; labels stream out
                     else
-                        tma_store_3d(&tm_lab, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg);
+                        tma_store_3d(tmap, int(x0 + wc * 32), int(y0 + wy * 32), int(ti.fz), stg);
                 }
             }
         }
@@ -1551,6 +1604,12 @@ __global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constan
         __syncthreads();  // stage buffers j1 / j2 are free for thread 0's next copies
     }
     if (TMA_ST && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+template <class C, bool RUNS, bool TMA_ST, bool BAND>
+__global__ void __launch_bounds__(C::NT, CCL_EMINB) k_final(const __grid_constant__ CUtensorMap tm_lab, uint32_t* L,
+                                                    const uint32_t* work, Geo g, uint32_t ntiles) {
+    final_tiles<C, RUNS, TMA_ST, BAND>(&tm_lab, L, work, g, ntiles, blockIdx.x, gridDim.x);
 }
 
 // ================================================================== host side
