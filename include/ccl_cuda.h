@@ -67,8 +67,12 @@ void* ccl_ctx_stream(ccl_ctx* ctx);
 ccl_status ccl_label_device(ccl_ctx* ctx, const uint8_t* d_img, size_t img_pitch, uint32_t w, uint32_t h,
                             uint32_t* d_labels, int variant, void* stream, int sync, ccl_timing* timing);
 
-/* Host path used by ccl::label_image: H2D (pinned staging), the kernels, D2H.
- * Blocking.  `kernel_ms` (may be NULL) = device time of the kernels only. */
+/* Host path used by ccl::label_image: H2D, the kernels, D2H.  Blocking.
+ * Page-locked img / labels are copied directly; pageable ones (std::vector,
+ * numpy) are staged through the context's page-locked double buffer in 16 MiB
+ * chunks, the host-side copy of one chunk (split over a small thread pool)
+ * overlapping the DMA of the other, in both directions.
+ * `kernel_ms` (may be NULL) = device time of the kernels only. */
 ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels,
                           int variant, float* kernel_ms);
 /* The same, asynchronous: H2D, kernels and D2H are enqueued on ctx's stream

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <exception>
 #include <stdexcept>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 
@@ -448,9 +449,147 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     return CCL_OK;
 }
 
+namespace {
+
+bool page_locked(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Host memcpy split over a small persistent worker pool (the pageable side of
+// the staged copies below: one thread copies ~10 GB/s, PCIe moves ~50 GB/s).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool* pool = new CopyPool();  // never destroyed (workers are detached)
+        return *pool;
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        const size_t parts = n < (size_t(1) << 20) ? 1 : workers_ + 1;
+        if (parts == 1) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        const size_t step = (n / parts + 63) & ~size_t(63);
+        std::unique_lock<std::mutex> lk(mu_);
+        for (size_t k = 1; k < parts; ++k) {
+            const size_t off = std::min(n, k * step), len = std::min(step, n - off);
+            jobs_.push_back({static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len});
+        }
+        pending_ += parts - 1;
+        lk.unlock();
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(step, n));  // the caller's own share
+        lk.lock();
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+private:
+    struct Job {
+        char* d;
+        const char* s;
+        size_t n;
+    };
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        workers_ = std::max(1u, std::min(7u, hw > 2 ? hw / 2 : 1u));
+        for (unsigned i = 0; i < workers_; ++i) std::thread([this] { run(); }).detach();
+    }
+    void run() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return !jobs_.empty(); });
+            const Job j = jobs_.back();
+            jobs_.pop_back();
+            lk.unlock();
+            std::memcpy(j.d, j.s, j.n);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    unsigned workers_ = 1;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    std::vector<Job> jobs_;
+    size_t pending_ = 0;
+};
+
+}  // namespace
+
+// Blocking host path of ccl::label_image.  Page-locked buffers go straight to
+// the copy engines; PAGEABLE ones (std::vector, numpy) are staged through the
+// context's page-locked double buffer in 16 MiB chunks, the host copy of one
+// chunk overlapping the DMA of the other (both directions).
 ccl_status ccl_label_host(ccl_ctx* ctx, const uint8_t* img, uint32_t w, uint32_t h, uint32_t* labels, int variant,
                           float* kernel_ms) {
-    if (ccl_status s = ccl_label_host_async(ctx, img, w, h, labels, variant)) return s;
+    if (!ctx || !img || !labels) return fail(CCL_EINVAL, "null argument");
+    if (ccl_status s = check_dims(w, h)) return s;
+    if (variant < 0 || variant > 3) return fail(CCL_EINVAL, "unknown variant");
+    DeviceGuard dg(ctx->device);
+    if (page_locked(img) && page_locked(labels)) {
+        if (ccl_status s = ccl_label_host_async(ctx, img, w, h, labels, variant)) return s;
+    } else {
+        const size_t pitch = (size_t(w) + 15) / 16 * 16;
+        const size_t img_bytes = pitch * h, lab_bytes = size_t(w) * h * 4;
+        if (ctx->d_img_bytes < img_bytes) {
+            if (ctx->d_img) cudaFree(ctx->d_img);
+            ctx->d_img = nullptr;
+            ctx->d_img_bytes = 0;
+            CCL_CHECK(cudaMalloc(&ctx->d_img, img_bytes));
+            ctx->d_img_bytes = img_bytes;
+        }
+        if (ctx->d_lab_bytes < lab_bytes) {
+            if (ctx->d_lab) cudaFree(ctx->d_lab);
+            ctx->d_lab = nullptr;
+            ctx->d_lab_bytes = 0;
+            CCL_CHECK(cudaMalloc(&ctx->d_lab, lab_bytes));
+            ctx->d_lab_bytes = lab_bytes;
+        }
+        constexpr size_t CH = size_t(16) << 20;
+        if (!ctx->h_ring) {
+            CCL_CHECK(cudaMallocHost(&ctx->h_ring, 2 * CH));
+            for (auto& e : ctx->ring_ev) CCL_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        CopyPool& pool = CopyPool::get();
+        cudaStream_t st = ctx->stream;
+        // H2D: rows_per_chunk rows per slot
+        const uint32_t rpc = uint32_t(std::max<size_t>(1, CH / w));
+        bool slot_busy[2] = {false, false};
+        for (uint32_t r0 = 0, i = 0; r0 < h; r0 += rpc, ++i) {
+            const uint32_t rows = std::min(rpc, h - r0);
+            const int k = int(i & 1u);
+            if (slot_busy[k]) CCL_CHECK(cudaEventSynchronize(ctx->ring_ev[k]));  // its previous DMA has read it
+            pool.copy(ctx->h_ring + k * CH, img + size_t(r0) * w, size_t(rows) * w);
+            CCL_CHECK(cudaMemcpy2DAsync(ctx->d_img + size_t(r0) * pitch, pitch, ctx->h_ring + k * CH, w, w, rows,
+                                        cudaMemcpyHostToDevice, st));
+            CCL_CHECK(cudaEventRecord(ctx->ring_ev[k], st));
+            slot_busy[k] = true;
+        }
+        if (ccl_status s = ccl_label_device(ctx, ctx->d_img, pitch, w, h, ctx->d_lab, variant, st, 0, nullptr))
+            return s;
+        // D2H: the DMA of chunk j+1 runs while chunk j is copied out
+        const size_t nch = (lab_bytes + CH - 1) / CH;
+        auto issue = [&](size_t j) -> cudaError_t {
+            const size_t off = j * CH, n = std::min(CH, lab_bytes - off);
+            cudaError_t e = cudaMemcpyAsync(ctx->h_ring + (j & 1) * CH, reinterpret_cast<uint8_t*>(ctx->d_lab) + off, n,
+                                            cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[j & 1], st);
+            return e;
+        };
+        CCL_CHECK(cudaEventSynchronize(ctx->ring_ev[0]));  // the H2D slots are free again
+        CCL_CHECK(cudaEventSynchronize(ctx->ring_ev[1]));
+        CCL_CHECK(issue(0));
+        for (size_t j = 0; j < nch; ++j) {
+            if (j + 1 < nch) CCL_CHECK(issue(j + 1));
+            CCL_CHECK(cudaEventSynchronize(ctx->ring_ev[j & 1]));
+            const size_t off = j * CH, n = std::min(CH, lab_bytes - off);
+            pool.copy(reinterpret_cast<uint8_t*>(labels) + off, ctx->h_ring + (j & 1) * CH, n);
+        }
+    }
     CCL_CHECK(cudaStreamSynchronize(ctx->stream));
     ccl_timing t{};
     if (ccl_status s = read_timing(ctx, &t)) return s;
