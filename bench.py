@@ -44,6 +44,9 @@ sys.path.insert(0, REPO)
 
 BYTES_PER_PX = 5  # algorithmic: 1 B u8 image in + 4 B u32 label out
 METRIC = "Gpixels/s labeled (8192^2 random binary, d=0.5)"
+METRICS = {"random8192": METRIC,
+           "strips32768": "Gpixels/s labeled (32768^2 random d=0.5, strip-partitioned)",
+           "batch1080": "Gpixels/s labeled (1024 x 1920x1080 random d=0.5 frames)"}
 DATA = "synthetic (reference xoshiro256** generator / reference patterns)"
 SWEEP = [0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9]
 PATTERNS = ["blobs", "spiral", "stripes", "checkerboard"]
@@ -246,7 +249,7 @@ def run_reference_impl(args):
                    else "oracle sequential_ccl port, 1 thread"))
         cfg = {"workload": workload, "width": W_, "height": H_, "density": 0.5, "seed": 0}
     val = px / mean_s / 1e9
-    line = {"metric": METRIC if workload == "random8192" else f"Gpixels/s labeled ({workload})", "value": val,
+    line = {"metric": METRICS.get(workload, f"Gpixels/s labeled ({workload})"), "value": val,
             "unit": "Gpixels/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
             "scaling": "weak" if workload == "random8192" else "strong", "vs_baseline": None, "dtype": "u32",
@@ -491,7 +494,7 @@ def main():
                "strips": ws, "rows_per_gpu": lab.h, "variant": args.variant,
                "exchange": "in-library: 16*W-byte seam export stored into every rank's exchange area "
                            "(CUDA IPC, NVLink peer stores) + device epoch flags; no host round trip"}
-        metric = "Gpixels/s labeled (32768^2 random d=0.5, strip-partitioned)"
+        metric = METRICS["strips32768"]
     elif workload == "batch1080":
         w, h, total = 1920, 1080, 1024
         per = total // ws + (1 if rank < total % ws else 0)
@@ -504,7 +507,7 @@ def main():
         px_step, scaling = total * w * h, "strong"
         cfg = {"workload": "batch1080", "width": w, "height": h, "frames": total, "frames_per_gpu": per,
                "density": 0.5, "seeds": "0..1023", "variant": args.variant}
-        metric = "Gpixels/s labeled (1024 x 1920x1080 random d=0.5 frames)"
+        metric = METRICS["batch1080"]
     else:  # single-GPU config lines
         key = {"sweep2048": "2_sweep2048", "patterns8192": "3_8192", "parity512": "1_parity512"}[workload]
         table = measure_single(ccl, timer, ctx, dev, stream, workload, args)
