@@ -292,16 +292,33 @@ class Timer:
         return statistics.mean(a.elapsed_time(b) for a, b in zip(ev0, ev1))
 
 
-def measure_configs(ccl, timer, ctx, dev, stream, steps=5, warmup=3):
+def cpu_ref_gpx(img_np, reps=3):
+    """Reference CPU labeler (oracle/_ref, all host cores) on one image: Gpx/s, median of `reps`."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    n = os.cpu_count() or 1
+    ms = _median_ms(lambda: oracle.ref_label_image(img_np, 32, 32, "c2fl", n)[1], reps)
+    return img_np.size / (ms * 1e-3) / 1e9
+
+
+def measure_configs(ccl, timer, ctx, dev, stream, steps=5, warmup=3, cpu=True):
     """Every other north_star config on this GPU, device-resident, L2 flushed
-    between steps (per-config throughput visible in the driver's bench line)."""
+    between steps (per-config throughput visible in the driver's bench line),
+    each with the reference CPU labeler's throughput on the same image beside
+    it (`cpu_gpx_s`, all host cores; 32768^2: its first 2048 rows)."""
+    import numpy as np
     import torch
     out = {}
 
     def one(img, w, h):
         lab = torch.empty((h, w), dtype=torch.uint32, device=dev)
         ms = timer.run(lambda: ccl.label_device(img, lab, stream=stream, ctx=ctx), steps, warmup)
-        return {"ms": ms, "gpx_s": w * h / (ms * 1e-3) / 1e9}
+        r = {"ms": ms, "gpx_s": w * h / (ms * 1e-3) / 1e9}
+        if cpu:
+            host = img.cpu().numpy() if h <= 8192 else np.ascontiguousarray(img[:2048].cpu().numpy())
+            r["cpu_gpx_s"] = cpu_ref_gpx(host)
+        return r
 
     img = ccl.random_image_device(512, 512, 0.5, 0, device=dev.index)
     out["1_parity512"] = one(img, 512, 512)
@@ -575,7 +592,7 @@ def main():
             if not args.no_cpu_baseline:
                 line["cpu_baseline"] = cpu_baseline(img_np)
             if not args.no_configs:
-                line["configs"] = measure_configs(ccl, timer, ctx, dev, stream)
+                line["configs"] = measure_configs(ccl, timer, ctx, dev, stream, cpu=not args.no_cpu_baseline)
                 if not args.no_cpu_baseline:
                     line["configs"]["4_batch1080"]["cpu_baseline"] = cpu_baseline_batch()
     if workload != "random8192":  # e2e through the host API on every rank, max over ranks
