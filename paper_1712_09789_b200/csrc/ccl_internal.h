@@ -40,6 +40,9 @@
 #ifndef CCL_SEAM_K
 #define CCL_SEAM_K 4  // kernel (d): 32-pair seam chunks per warp (unions compacted over the warp)
 #endif
+#ifndef CCL_MARKRUN
+#define CCL_MARKRUN 1  // band kernel (a): seam-root marks from one dense list of border-run starts
+#endif
 #ifndef CCL_BJUMP
 #define CCL_BJUMP 1  // band kernel (a): pointer-jumping rounds before the unions
 #endif

@@ -1116,12 +1116,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
         static_assert(C::NT == C::TW && C::NT == 2 * C::TH, "one top, one bottom and one side item per thread");
-#pragma unroll
-        for (int s3 = 0; s3 < 3; ++s3) {
-            const int i = s3 * C::NT + tid;  // top, bottom, then left / right
-            const bool act = s3 == 0 ? has_top : s3 == 1 ? has_bot : (tid < C::TH ? has_left : has_right);
-            uint32_t x = BN[i];
-            if (!act || x == 0xFFFFu) continue;
+        auto mark = [&](uint32_t x) {  // x: the node of a foreground pixel on a facing side
             uint32_t p = P[x];
             while (!(p & kRoot)) {
                 mc.step();
@@ -1137,7 +1132,48 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 FR[1 + k] = n;
                 P[x] = node_t(kRoot | kSeam | k);
             }
+        };
+#if CCL_MARKRUN
+        {   // one item per RUN of foreground pixels along a facing side (the run's
+            // pixels are adjacent, so they share the root): each warp lists its
+            // run starts (ballots), then the whole CTA walks the dense list
+            // (~100 items instead of 384 pixel slots, 3 per thread)
+            uint32_t* WL = reinterpret_cast<uint32_t*>(smem + A::UL_OFF) + warp * A::UL_CAP;  // dead after the unions
+            uint16_t* WLi = reinterpret_cast<uint16_t*>(WL + 1);
+            static_assert(2 * (A::UL_CAP - 1) >= 3 * 32, "one warp's run starts fit in its union list");
+            uint32_t nw = 0;
+#pragma unroll
+            for (int s3 = 0; s3 < 3; ++s3) {
+                const int i = s3 * C::NT + tid;  // top, bottom, then left / right
+                const bool act = s3 == 0 ? has_top : s3 == 1 ? has_bot : (tid < C::TH ? has_left : has_right);
+                const bool first = s3 < 2 ? tid == 0 : (tid & (C::TH - 1)) == 0;  // first pixel of its side
+                const bool st = act && BN[i] != 0xFFFFu && (first || BN[i - 1] == 0xFFFFu);
+                const uint32_t bal = __ballot_sync(0xffffffffu, st);
+                if (st) WLi[nw + __popc(bal & ((1u << lane) - 1u))] = uint16_t(i);
+                nw += __popc(bal);
+            }
+            if (lane == 0) WL[0] = nw;
+            __syncthreads();
+            static_assert(C::NWARP == 4, "four warp lists");
+            const uint32_t* UL0 = reinterpret_cast<const uint32_t*>(smem + A::UL_OFF);
+            const uint32_t e1 = UL0[0], e2 = e1 + UL0[A::UL_CAP], e3 = e2 + UL0[2 * A::UL_CAP],
+                           e4 = e3 + UL0[3 * A::UL_CAP];  // list ends (exclusive prefix of the warp counts)
+            for (uint32_t j = tid; j < e4; j += C::NT) {
+                const uint32_t w = uint32_t(j >= e1) + uint32_t(j >= e2) + uint32_t(j >= e3);
+                const uint32_t b = w == 0 ? 0u : w == 1 ? e1 : w == 2 ? e2 : e3;
+                const uint16_t* li = reinterpret_cast<const uint16_t*>(UL0 + w * A::UL_CAP + 1);
+                mark(BN[li[j - b]]);
+            }
         }
+#else
+#pragma unroll
+        for (int s3 = 0; s3 < 3; ++s3) {
+            const int i = s3 * C::NT + tid;  // top, bottom, then left / right
+            const bool act = s3 == 0 ? has_top : s3 == 1 ? has_bot : (tid < C::TH ? has_left : has_right);
+            const uint32_t x = BN[i];
+            if (act && x != 0xFFFFu) mark(x);
+        }
+#endif
         __syncthreads();
         CCL_PH(12);
 
