@@ -226,9 +226,10 @@ ccl_status run_pipeline(ccl_ctx* ctx, cclk::LaunchArgs& a, bool events, bool spl
 #endif
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[0], a.stream));
     a.g.epoch = next_epoch();
-    CCL_CHECK(cclk::launch_local(a));
+    const int skip = cclk::debug_skip();
+    if (!(skip & 1)) CCL_CHECK(cclk::launch_local(a));
     if (ctx->last_split) CCL_CHECK(cudaEventRecord(ctx->ev[1], a.stream));
-    CCL_CHECK(cclk::launch_seams(a));
+    if (!(skip & 2)) CCL_CHECK(cclk::launch_seams(a));
     if (ctx->last_split) CCL_CHECK(cudaEventRecord(ctx->ev[2], a.stream));
     CCL_CHECK(cclk::launch_final(a));
     if (events) CCL_CHECK(cudaEventRecord(ctx->ev[3], a.stream));

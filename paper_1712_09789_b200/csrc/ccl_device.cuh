@@ -55,6 +55,15 @@ __device__ __forceinline__ uint32_t eq1_nibble(uint32_t v) {
 __device__ __forceinline__ uint32_t eq1_mask16(uint4 q) {
     return eq1_nibble(q.x) | (eq1_nibble(q.y) << 4) | (eq1_nibble(q.z) << 8) | (eq1_nibble(q.w) << 12);
 }
+// Same for a chunk whose bytes are all 0 or 1 (the caller checks): byte k's
+// low bit gathered to bit k of each nibble by one multiply per word
+// (bits 21-24 of v * 0x00204081 are exactly b0..b3; the cross terms land on
+// bits 0-16 and 29-31 and cannot carry into them).
+__device__ __forceinline__ uint32_t bin_mask16(uint4 q) {
+    constexpr uint32_t G = 0x00204081u;
+    return (((q.x * G) >> 21) & 0xFu) | (((q.y * G) >> 17) & 0xF0u) | (((q.z * G) >> 13) & 0xF00u) |
+           (((q.w * G) >> 9) & 0xF000u);
+}
 // Highest set bit of s at or below bit b (caller guarantees one exists).
 __device__ __forceinline__ uint32_t hi_bit_le(uint32_t s, uint32_t b) {
     return 31u - __clz(s & (0xFFFFFFFFu >> (31u - b)));

@@ -64,6 +64,12 @@
 #ifndef CCL_BMINB
 #define CCL_BMINB 12  // min resident CTAs of the band kernel (a)
 #endif
+#ifndef CCL_BINFAST
+#define CCL_BINFAST 1  // kernel (a): multiply-gather masks when every byte of a warp's chunks is 0 or 1
+#endif
+#ifndef CCL_SEAM_NOUNION
+#define CCL_SEAM_NOUNION 0  // timing probe: kernel (d) skips its unions (wrong labels)
+#endif
 #ifndef CCL_PHASES
 #define CCL_PHASES 0
 #endif
@@ -120,6 +126,8 @@ struct LaunchArgs {
 };
 
 cudaError_t launch_local(const LaunchArgs& a);
+// timing ablations only (env CCL_DEBUG_SKIP, bits: 1 (a), 2 (d), 4 (d2), 8 (e)); labels are wrong when set
+int debug_skip();
 cudaError_t launch_seams(const LaunchArgs& a);
 cudaError_t launch_final(const LaunchArgs& a);
 

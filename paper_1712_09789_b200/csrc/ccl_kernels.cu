@@ -887,10 +887,20 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
 #pragma unroll
             static_assert((C::TH * CPR) % C::NT == 0, "whole mask-build rounds");
-            for (int kk = 0; kk < C::TH * CPR / C::NT; ++kk) {
-                const int c = kk * C::NT + tid;
-                const uint4 q = *reinterpret_cast<const uint4*>(IMG + c * 16);
-                M16[c] = static_cast<uint16_t>(eq1_mask16(q));
+            constexpr int KK = C::TH * CPR / C::NT;
+            uint4 q[KK];
+            uint32_t big = 0u;  // any byte > 1 in this thread's chunks
+#pragma unroll
+            for (int kk = 0; kk < KK; ++kk) {
+                q[kk] = *reinterpret_cast<const uint4*>(IMG + (kk * C::NT + tid) * 16);
+                big |= (q[kk].x | q[kk].y | q[kk].z | q[kk].w) & 0xFEFEFEFEu;
+            }
+            if (CCL_BINFAST && !__any_sync(0xffffffffu, big)) {  // 0/1 images: one multiply per word
+#pragma unroll
+                for (int kk = 0; kk < KK; ++kk) M16[kk * C::NT + tid] = static_cast<uint16_t>(bin_mask16(q[kk]));
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < KK; ++kk) M16[kk * C::NT + tid] = static_cast<uint16_t>(eq1_mask16(q[kk]));
             }
         } else {  // unaligned pitch: byte loads, one mask word per thread and step
             for (int i = tid; i < C::MW; i += C::NT) {
@@ -1350,7 +1360,11 @@ __device__ __forceinline__ void seams_warp(uint32_t* work, const Geo& g, uint32_
     __syncwarp();
     for (uint32_t j = lane; j < n; j += 32) {
         const uint2 pr = list[j];
+#if CCL_SEAM_NOUNION  // timing probe only: wrong labels
+        if (pr.x == 0xFFFFFFF0u) fst.f[0] = pr.y;
+#else
         fst.unite(pr.x, pr.y, mc);
+#endif
     }
     __syncwarp();  // the list is reused by this warp's next share (fused kernel)
     metrics_phase(g, 0, mc);
@@ -1760,15 +1774,26 @@ cudaError_t launch_local(const LaunchArgs& a) {
     }
 }
 
+int debug_skip() {
+    static const int v = [] {
+        const char* e = std::getenv("CCL_DEBUG_SKIP");
+        return e && *e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <bool RUNS, bool BAND>
 static cudaError_t launch_final_v(const LaunchArgs& a) {
     using C = typename std::conditional<BAND, BandECfg, ECfg>::type;
     using E = ELayout<C, RUNS, BAND>;
     const uint32_t nt = tile_count(a);
     constexpr int NTH = C::NT;
-    cudaError_t e = launch_ex(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream,
-                              !a.no_pdl_first, a.work, a.g, nt);
+    cudaError_t e = cudaSuccess;
+    if (!(debug_skip() & 4))
+        e = launch_ex(k_resolve<TileCfg>, dim3(unsigned((uint64_t(nt) * 32 + 255) / 256)), 256, 0, a.stream,
+                      !a.no_pdl_first, a.work, a.g, nt);
     if (e != cudaSuccess) return e;
+    if (debug_skip() & 8) return cudaGetLastError();
     if (a.tma_store) {
         auto k = k_final<C, RUNS, true, BAND>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, E::SMEM);
