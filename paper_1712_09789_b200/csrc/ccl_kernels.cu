@@ -1015,30 +1015,23 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t contp = bs[k] ? (1u << (lowbit(bs[k]))) - 1u : 0xFFFFFFFFu;
             const uint32_t firstm = seg_first(o, bs[k]) & ~contp;   // first overlap of each band run
             const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
-            {   // a band run without a top-row pixel: a root coded by its first column
-                uint32_t tt = bs[k] & ~seg_back(tfirst, bs[k]);
-                while (tt) {
-                    const uint32_t a = lowbit(tt);
-                    tt &= tt - 1;
-                    P[node_of(pfx[k], bs[k], a)] = node_t(kRoot | (rowpos1 + a));
+            {   // linked runs: one trip per first overlap (the run holding it
+                // links to the band run above holding it); roots: one trip per
+                // run without an overlap, coded by its first top-row pixel or,
+                // without one, by its first column in the bottom row
+                uint32_t ff = firstm;
+                while (ff) {
+                    const uint32_t f = lowbit(ff);
+                    ff &= ff - 1;
+                    P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
                 }
-            }
-            {   // with one: coarse link to the band run above holding its first
-                // overlap (o is inside tm: the run's first overlap, when it has one,
-                // precedes the next run's first top-row pixel), else a root coded by
-                // its first top-row pixel
-                uint32_t tt = tfirst, ff = firstm;
-                while (tt) {
-                    const uint32_t f = lowbit(tt);
-                    tt &= tt - 1;
-                    uint32_t v = kRoot | (rowpos0 + f);
-                    // lowest overlap before the next run's first top pixel (an empty
-                    // mask's isolated low bit - 1 wraps to "infinity")
-                    if ((ff & (0u - ff)) - 1u < (tt & (0u - tt)) - 1u) {
-                        v = node_of(upfx[k], ubs[k], lowbit(ff));
-                        ff &= ff - 1;
-                    }
-                    P[node_of(pfx[k], bs[k], f)] = node_t(v);
+                const uint32_t top_root = tfirst & ~seg_back(firstm, bs[k]);  // first top pixels of unlinked runs
+                uint32_t rr = top_root | (bs[k] & ~seg_back(tfirst, bs[k]));  // ... and starts of runs without one
+                while (rr) {
+                    const uint32_t a = lowbit(rr);
+                    rr &= rr - 1;
+                    const uint32_t pos = (((top_root >> a) & 1u) ? rowpos0 : rowpos1) + a;
+                    P[node_of(pfx[k], bs[k], a)] = node_t(kRoot | pos);
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));

@@ -1,5 +1,5 @@
 """A/B timing of experiment libraries (graph-replayed device path, L2 flushed
-between steps, median of 15), each library in its own process, with a
+between steps, trimmed mean of 15), each library in its own process, with a
 bit-exactness check against the oracle.
 usage: CMP_IMGS=d0.5,zeros,... python scripts/cmp_libs.py lib1.so lib2.so ..."""
 import os
@@ -44,11 +44,12 @@ def child(names, n, check):
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
         ts.sort()
+        ts = ts[3:-3]
         _, t = ccl.label_device(img, out, sync=True)
         ok = ""
         if check:
             ok = " OK" if np.array_equal(out.cpu().numpy(), oracle.sequential_ccl(img_np)) else " MISMATCH"
-        out_lines.append(f"{name}:{ts[len(ts) // 2]:.1f}(a{t['local_ms'] * 1e3:.0f}){ok}")
+        out_lines.append(f"{name}:{sum(ts) / len(ts):.1f}(a{t['local_ms'] * 1e3:.0f}){ok}")
     print("  ".join(out_lines))
 
 
