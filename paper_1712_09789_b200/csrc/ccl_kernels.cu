@@ -1440,6 +1440,8 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
     uint8_t* smem = aligned_smem();
     uint64_t* b1 = reinterpret_cast<uint64_t*>(smem + E::BAR_OFF);
     uint64_t* b2 = b1 + 3;
+    uint64_t* b3 = b1 + 5;  // second half of an oversized band table
+    uint32_t b3par = 0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wx = warp % C::WX, wy = warp / C::WX;
     const int row = wy * 32 + lane;
@@ -1450,9 +1452,17 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
         mbar_expect_tx(&b1[j], E::S1B);
         bulk_load(s1buf(j), work_tile<C>(const_cast<uint32_t*>(work), t), E::S1B, &b1[j]);
     };
+    // a band tile with more nodes than the stage holds (checkerboard-like) is
+    // staged in two halves: bands 0-15 first, bands 16-31 after them
+    // (<= 16 x 4 x 32 = 2048 nodes each)
+    static_assert(!BAND || 16 * C::WPR * 32 + 8 <= E::TBLN, "half a band tile's table fits the stage");
+    auto half_nodes = [&](const uint32_t* head) -> uint32_t {
+        return reinterpret_cast<const uint16_t*>(head + 4 + C::MW)[16 * C::WPR];  // prefix of band 16
+    };
     auto s2 = [&](uint32_t t, uint32_t j, const uint32_t* head) {
         const uint32_t lb = (head[0] * 4 + 15) & ~15u;
-        const uint32_t tb = head[1] <= uint32_t(E::TBLN) ? (head[1] * 2 + 15) & ~15u : 0u;
+        const uint32_t tb = head[1] <= uint32_t(E::TBLN) ? (head[1] * 2 + 15) & ~15u
+                            : BAND ? (half_nodes(head) * 2 + 15) & ~15u : 0u;
         const uint32_t* wt = work_tile<C>(const_cast<uint32_t*>(work), t);
         mbar_expect_tx(&b2[j], lb + tb);
         if (lb) bulk_load(s2buf(j), wt + C::W_LIST, lb, &b2[j]);
@@ -1462,6 +1472,7 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
     if (tid == 0) {
         for (int j = 0; j < 3; ++j) mbar_init(&b1[j], 1);
         for (int j = 0; j < 2; ++j) mbar_init(&b2[j], 1);
+        mbar_init(b3, 1);
         const uint32_t t0 = cta;
         // heads / masks come from kernel (a), complete before (d2) let this grid
         // launch; only the seam labels of (d2) need the dependency wait.  Every
@@ -1510,9 +1521,12 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
         if constexpr (C::RPL == 2) {
             // (a lambda called once per table location, so the shared-memory
             // table keeps LDS and the global fallback uses LDG)
-            auto expand = [&](const uint16_t* tbl) {
+            auto expand = [&](const uint16_t* tbl, int lo, int hi) {
             // lane = band (rows 2b, 2b+1) of word column wx: the band starts are
-            // walked once and both rows are filled (two 32x32 staging tiles per warp)
+            // walked once and both rows are filled (two 32x32 staging tiles per
+            // warp); lanes [lo, hi) only, then their staging tiles are stored
+            static_assert(C::WY == 1, "lane = band of the whole tile");
+            if (lane >= lo && lane < hi) {
             const int b = wy * 32 + lane, wc = wx;
             const int r0 = 2 * b, r1 = r0 + 1;
             const int k = (r0 >> 5) & 1;  // staging tile of both rows (this warp covers rows 64 wy .. 64 wy + 63)
@@ -1561,20 +1575,36 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
                     }
                 }
             }
+            }
             if (TMA_ST) {
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    for (int kk = 0; kk < 2; ++kk) {
+                    for (int kk = lo / 16; kk < (hi + 15) / 16; ++kk) {
                         uint8_t* sk = smem + E::STG_OFF + (warp * 2 + kk) * 4096;
-                        tma_store_3d_hint(tmap, int(x0 + wc * 32), int(y0 + 64 * wy + 32 * kk), int(ti.fz), sk,
+                        tma_store_3d_hint(tmap, int(x0 + wx * 32), int(y0 + 64 * wy + 32 * kk), int(ti.fz), sk,
                                           policy_evict_first());
                     }
                 }
             }
             };
-            if (M[-4 + 1] <= uint32_t(E::TBLN)) expand(TBL);
-            else expand(reinterpret_cast<const uint16_t*>(work_tile<C>(const_cast<uint32_t*>(work), t) + C::W_TBL));
+            if (M[-4 + 1] <= uint32_t(E::TBLN)) {
+                expand(TBL, 0, 32);
+            } else {  // two halves through the stage: bands 0-15, then bands 16-31
+                expand(TBL, 0, 16);
+                const uint32_t h = half_nodes(M - 4), a0 = (h * 2) & ~15u;  // 16-byte aligned source
+                __syncthreads();  // every warp is done with the first half
+                if (tid == 0) {
+                    const uint32_t bytes = (M[-4 + 1] * 2 - a0 + 15) & ~15u;
+                    mbar_expect_tx(b3, bytes);
+                    bulk_load(const_cast<uint16_t*>(TBL),
+                              reinterpret_cast<const uint8_t*>(work_tile<C>(const_cast<uint32_t*>(work), t) + C::W_TBL) + a0,
+                              bytes, b3);
+                }
+                mbar_wait(b3, b3par);
+                b3par ^= 1u;
+                expand(TBL - a0 / 2, 16, 32);
+            }
         } else {
 #pragma unroll 1
         for (int k = 0; k < C::WPL; ++k) {  // this lane's row words, one 32x32 staging tile each
