@@ -184,11 +184,11 @@ ccl_status prepare(cclk::LaunchArgs* a, const uint8_t* img, size_t pitch, size_t
 }
 
 // CUDA graphs for repeated device-path calls (off with CCL_GRAPHS=0; never in
-// instrumented or fused-seam builds: per-call memsets / launch epochs).
+// instrumented builds: per-call memsets).
 bool graphs_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("CCL_GRAPHS");
-        return !(v && v[0] == '0') && !CCL_METRICS && !CCL_FUSE_SEAMS;
+        return !(v && v[0] == '0') && !CCL_METRICS;
     }();
     return on;
 }
@@ -404,7 +404,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     const uint32_t tiles_per_frame = ((w + cclk::tile_w() - 1) / cclk::tile_w()) * ((h + cclk::tile_h() - 1) / cclk::tile_h());
     const uint32_t min_chunk_tiles = uint32_t(env_int("CCL_PIPE_TILES", 16384));
     const uint32_t chunk = std::max(1u, (min_chunk_tiles + tiles_per_frame - 1) / tiles_per_frame);
-    const bool pipe = env_int("CCL_PIPE", 1) != 0 && n >= 3 * chunk && !CCL_METRICS && !CCL_FUSE_SEAMS;
+    const bool pipe = env_int("CCL_PIPE", 1) != 0 && n >= 3 * chunk && !CCL_METRICS;
     if (!pipe) {
         cclk::LaunchArgs a{};
         if (ccl_status s = make_geo(w, h, 0, img_pitch, frame_pitch, false, false, &a.g)) return s;

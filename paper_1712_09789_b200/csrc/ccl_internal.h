@@ -34,23 +34,14 @@
 #ifndef CCL_ETBL
 #define CCL_ETBL 3072  // band kernel (e): node-table stage capacity (sized for 4 CTAs/SM)
 #endif
-#ifndef CCL_FUSE_SEAMS
-#define CCL_FUSE_SEAMS 0  // band kernel (a) unions each tile seam itself (second finisher); no kernel (d)
-#endif
 #ifndef CCL_SEAM_K
 #define CCL_SEAM_K 4  // kernel (d): 32-pair seam chunks per warp (unions compacted over the warp)
-#endif
-#ifndef CCL_MARKRUN
-#define CCL_MARKRUN 1  // band kernel (a): seam-root marks from one dense list of border-run starts
 #endif
 #ifndef CCL_BJUMP
 #define CCL_BJUMP 1  // band kernel (a): pointer-jumping rounds before the unions
 #endif
 #ifndef CCL_METRICS
 #define CCL_METRICS 0  // instrumented build: per-tile find / CAS counters (separate library)
-#endif
-#ifndef CCL_ABAL
-#define CCL_ABAL 0  // band kernel (a): persistent grid sized so every CTA walks the same number of tiles
 #endif
 #ifndef CCL_AIMG_OVERLAY
 #define CCL_AIMG_OVERLAY 1  // band kernel (a): TMA tile staged in the node table (no prefetch, -8 KB smem)

@@ -1136,7 +1136,6 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 P[x] = node_t(kRoot | kSeam | k);
             }
         };
-#if CCL_MARKRUN
         {   // one item per RUN of foreground pixels along a facing side (the run's
             // pixels are adjacent, so they share the root): each warp lists its
             // run starts (ballots), then the whole CTA walks the dense list
@@ -1168,15 +1167,6 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 mark(BN[li[j - b]]);
             }
         }
-#else
-#pragma unroll
-        for (int s3 = 0; s3 < 3; ++s3) {
-            const int i = s3 * C::NT + tid;  // top, bottom, then left / right
-            const bool act = s3 == 0 ? has_top : s3 == 1 ? has_bot : (tid < C::TH ? has_left : has_right);
-            const uint32_t x = BN[i];
-            if (act && x != 0xFFFFu) mark(x);
-        }
-#endif
         __syncthreads();
         CCL_PH(12);
 
@@ -1226,38 +1216,6 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 if (gx < g.W) SE[(s3 == 0 ? 0u : g.W) + gx] = v;
             }
         }
-#if CCL_FUSE_SEAMS
-        // ---- kernel (d) fused: with this tile's records and seam roots published,
-        // each internal seam is unioned by whichever of its two tiles finishes
-        // second (epoch exchange on the seam's flag; nobody waits)
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();  // cumulative over the barrier: publishes the whole CTA's stores
-            const uint32_t ep = g.epoch;
-            uint32_t todo = 0;
-            if (ty > 0 && atomicExch(work_tile<C>(work, t - g.ntx) + C::W_HEAD + 2, ep) == ep) todo |= 1u;
-            if (ty + 1 < g.nty && atomicExch(wt + C::W_HEAD + 2, ep) == ep) todo |= 2u;
-            if (tx > 0 && atomicExch(work_tile<C>(work, t - 1) + C::W_HEAD + 3, ep) == ep) todo |= 4u;
-            if (tx + 1 < g.ntx && atomicExch(wt + C::W_HEAD + 3, ep) == ep) todo |= 8u;
-            if (todo) __threadfence();
-            FR[0] = todo;
-        }
-        __syncthreads();
-        if (const uint32_t todo = FR[0]) {
-            constexpr uint32_t HC = C::TW / 32, VC = C::TH / 32;  // 32-pair chunks per seam
-            for (uint32_t j = warp; j < 2 * HC + 2 * VC; j += C::NWARP) {
-                const uint32_t s = j < HC ? 0u : j < 2 * HC ? 1u : j < 2 * HC + VC ? 2u : 3u;
-                if (!((todo >> s) & 1u)) continue;
-                const uint32_t c = s < 2 ? j - s * HC : j - 2 * HC - (s - 2) * VC;
-                const uint32_t *ra, *rb;  // (upper, lower) or (left, right) records
-                if (s == 0) { ra = work_tile<C>(work, t - g.ntx) + C::W_REC + C::TW; rb = wt + C::W_REC; }
-                else if (s == 1) { ra = wt + C::W_REC + C::TW; rb = work_tile<C>(work, t + g.ntx) + C::W_REC; }
-                else if (s == 2) { ra = work_tile<C>(work, t - 1) + C::W_REC + 2 * C::TW + C::TH; rb = wt + C::W_REC + 2 * C::TW; }
-                else { ra = wt + C::W_REC + 2 * C::TW + C::TH; rb = work_tile<C>(work, t + 1) + C::W_REC + 2 * C::TW; }
-                seam_chunk(fst, ra, rb, c, lane, mc);
-            }
-        }
-#endif
         metrics_tile(g, t, mc);
         if (TMA && A::OVL) {  // next tile into the node table once every reader is done with it
             fence_proxy_async_smem();
@@ -1714,13 +1672,6 @@ static unsigned persistent_grid(K kernel, int threads, int smem, uint32_t ntiles
 
 static uint32_t tile_count(const LaunchArgs& a) { return a.g.ntx * a.g.nty * a.nframes; }
 
-// Fewest CTAs that still finish in the same number of tile rounds: every CTA
-// then walks the same number of tiles (no half-empty last round).
-static unsigned balanced(unsigned grid, uint32_t ntiles) {
-    if (!CCL_ABAL || grid == 0 || ntiles <= grid) return grid;
-    const uint32_t rounds = (ntiles + grid - 1) / grid;
-    return unsigned((ntiles + rounds - 1) / rounds);
-}
 
 // Launch (optionally) with programmatic stream serialization: the kernel calls
 // pdl_wait() before reading what the previous kernel in the stream produced.
@@ -1775,7 +1726,7 @@ static cudaError_t launch_local_band(const LaunchArgs& a) {
         auto k = k_local_band<C, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, CCL_CARVEOUT);
-        e = launch_ex(k, dim3(balanced(persistent_grid(k, C::NT, A::SMEM, nt, a.a_cap_per_sm), nt)), C::NT, A::SMEM,
+        e = launch_ex(k, dim3(persistent_grid(k, C::NT, A::SMEM, nt, a.a_cap_per_sm)), C::NT, A::SMEM,
                       a.stream, false,
                       a.tm_img, a.img, a.work, a.g, nt);
     } else {
@@ -1839,7 +1790,6 @@ cudaError_t launch_final(const LaunchArgs& a) {
 
 cudaError_t launch_seams(const LaunchArgs& a) {
     using C = TileCfg;
-    if (CCL_FUSE_SEAMS && uses_band(a)) return cudaSuccess;  // kernel (a) did the seams
     const uint64_t chunks = uint64_t(a.g.nty - 1) * a.g.ntx * (C::TW / 32) + uint64_t(a.g.ntx - 1) * a.g.nty * (C::TH / 32);
     if (chunks == 0) return cudaSuccess;
     const uint64_t warps = (chunks + CCL_SEAM_K - 1) / CCL_SEAM_K;
