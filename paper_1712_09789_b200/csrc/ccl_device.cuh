@@ -123,6 +123,17 @@ struct Forest {
                      : "memory");
         return v;
     }
+    // L1-cached read for kernel (d2), which runs after every union (after its
+    // griddepcontrol.wait): a parent read stale from L1 -- another warp's path
+    // compression not yet seen -- is still an ancestor, keys never change.
+    // Near the percolation threshold every seam root of the spanning cluster
+    // climbs to the same few nodes; through L1 those lines are read once per
+    // SM instead of once per warp at one L2 slice (d=0.6: -7 us per step).
+    __device__ __forceinline__ uint2 node_ca(uint32_t n) const {
+        uint2 v;
+        asm volatile("ld.global.ca.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(f + 2 * size_t(n)) : "memory");
+        return v;
+    }
     __device__ __forceinline__ uint32_t key(uint32_t n) const { return node(n).y; }
     // Root of x and the root's {parent, key}.
     __device__ __forceinline__ uint32_t find(uint32_t x, uint2& v, Ctr& m) const {

@@ -1360,7 +1360,7 @@ __device__ __forceinline__ void resolve_tile(uint32_t* work, const Geo& g, uint3
                 if (k0 + lane + 32u * i < nf && v[i].x != cur[i]) {
                     mc.step();
                     cur[i] = v[i].x;
-                    v[i] = fst.node(cur[i]);
+                    v[i] = fst.node_ca(cur[i]);
                     more = true;
                 }
             if (!more) break;
