@@ -29,7 +29,7 @@
 #define CCL_EMINB 2
 #endif
 #ifndef CCL_BULCAP
-#define CCL_BULCAP 96  // band kernel union pairs per warp (sized for 10 resident CTAs per SM)
+#define CCL_BULCAP 160  // band kernel (a): union pairs per warp (dense tiles overflow 96: d=0.7 -20 us)
 #endif
 #ifndef CCL_ETBL
 #define CCL_ETBL 3072  // band kernel (e): node-table stage capacity (sized for 4 CTAs/SM)
