@@ -1484,6 +1484,14 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
             // walked once and both rows are filled (two 32x32 staging tiles per
             // warp); lanes [lo, hi) only, then their staging tiles are stored
             static_assert(C::WY == 1, "lane = band of the whole tile");
+            // bands whose runs start at the same columns (spirals, stripes,
+            // checkerboards: neighbouring bands with equal start masks) would hit
+            // one shared-memory bank all at once in the run-start scatter below;
+            // such warps walk their starts from a lane-rotated column (whole
+            // warp, before the lane range split)
+            const uint32_t st_w = BSt[(wy * 32 + lane) * C::WPR + wx];
+            const uint32_t st_n = __shfl_xor_sync(0xffffffffu, st_w, 1);  // every lane (no short circuit)
+            const bool rotw = __popc(__ballot_sync(0xffffffffu, st_w != 0u && st_n == st_w)) > 8;
             if (lane >= lo && lane < hi) {
             const int b = wy * 32 + lane, wc = wx;
             const int r0 = 2 * b, r1 = r0 + 1;
@@ -1496,7 +1504,19 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
             const uint32_t st = BSt[b * C::WPR + wc];
             const uint32_t pfx = PF16[b * C::WPR + wc];
             uint32_t cur = (!(st & 1u) && ((tm | um) & 1u)) ? lab_of(tbl[pfx - 1]) : kBG;
-            {
+            // run-start scatter into the staging row: rotated warps start at
+            // column 4 (lane & 7) and index the table by rank; the others keep
+            // the plain in-order walk (cheaper per run)
+            if (rotw) {
+                const uint32_t rot = 4u * (lane & 7);
+                uint32_t tt = __funnelshift_r(st, st, rot);
+                while (tt) {
+                    const uint32_t bb = ((__ffs(tt) - 1) + rot) & 31u;
+                    tt &= tt - 1;
+                    const uint32_t e = pfx + __popc(st & ((1u << bb) - 1u));
+                    *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(tbl[e]);
+                }
+            } else {
                 const uint16_t* e = tbl + pfx;
                 uint32_t tt = st;
                 while (tt) {

@@ -64,6 +64,10 @@ if __name__ == "__main__":
     for r in range(reps):
         for lib in sys.argv[1:]:
             env = dict(os.environ, CCL_LIB_PATH=lib)
-            p = subprocess.run([sys.executable, __file__, "--child", ",".join(names), str(n), check], env=env,
-                               capture_output=True, text=True)
+            try:
+                p = subprocess.run([sys.executable, __file__, "--child", ",".join(names), str(n), check], env=env,
+                                   capture_output=True, text=True, timeout=int(os.environ.get("CMP_TIMEOUT", "240")))
+            except subprocess.TimeoutExpired:
+                print(f"{os.path.basename(lib):36s} TIMEOUT", flush=True)
+                continue
             print(f"{os.path.basename(lib):36s} " + (p.stdout.strip() or p.stderr.strip()[-300:]), flush=True)
