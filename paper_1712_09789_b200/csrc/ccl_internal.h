@@ -20,7 +20,7 @@
 #define CCL_PDL 1  // programmatic dependent launch of kernels (d), (d2), (e)
 #endif
 #ifndef CCL_SEAM_MATCH
-#define CCL_SEAM_MATCH 1  // kernel (d): one union per distinct local-root pair per warp
+#define CCL_SEAM_MATCH 2  // kernel (d) dedup of a chunk's pairs: 1 = __match_any (distinct pairs), 2 = previous active pair
 #endif
 #ifndef CCL_CARVEOUT
 #define CCL_CARVEOUT 100  // preferred shared-memory carveout (%) of kernels (a) and (e)

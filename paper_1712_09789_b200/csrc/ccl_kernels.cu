@@ -801,28 +801,6 @@ __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b, Ct
     }
 }
 
-// Algorithm 2 on 32 pixel pairs of a seam (records ra / rb, chunk c): a pair
-// whose predecessor along the seam is also foreground on both sides joins the
-// same two local components and is skipped; one union per distinct (a, b)
-// pair of the warp.  Records are read at L2 (another CTA may have written them
-// in this launch).
-__device__ __forceinline__ void seam_chunk(const Forest& fst, const uint32_t* ra, const uint32_t* rb, uint32_t c,
-                                           int lane, Ctr& mc) {
-    const uint32_t i = c * 32 + lane;
-    const uint32_t a = __ldcg(ra + i), b = __ldcg(rb + i);
-    const bool fg = (a != kBG) && (b != kBG);
-    bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
-    if (lane == 0) prev = c > 0 && __ldcg(ra + i - 1) != kBG && __ldcg(rb + i - 1) != kBG;
-    bool act = fg && !prev;
-#if CCL_SEAM_MATCH
-    // the same two components often meet several times along 32 seam pixels
-    const uint64_t key = act ? (uint64_t(a) << 32 | b) : ~0ull;
-    const uint32_t same = __match_any_sync(0xffffffffu, key);
-    act = act && (__ffs(same) - 1 == lane);
-#endif
-    if (act) fst.unite(a, b, mc);
-}
-
 // Kernel (a) on band runs: CTA `cta` of `ncta` labels tiles cta, cta + ncta, ...
 // (the body of the persistent kernel below).
 template <class C, bool TMA>
@@ -1299,10 +1277,19 @@ __device__ __forceinline__ void seams_warp(uint32_t* work, const Geo& g, uint32_
         bool prev = __shfl_up_sync(0xffffffffu, fg, 1);
         if (lane == 0) prev = prev0[k];
         bool act = fg && !prev;
-#if CCL_SEAM_MATCH
+#if CCL_SEAM_MATCH == 1
         const uint64_t key = act ? (uint64_t(va[k]) << 32 | vb[k]) : ~0ull;
         const uint32_t same = __match_any_sync(0xffffffffu, key);
         act = act && (__ffs(same) - 1 == lane);
+#elif CCL_SEAM_MATCH == 2
+        {   // drop a pair equal to the previous active pair of the chunk (the
+            // same two components meeting again: dense images, long components)
+            const uint32_t ab = __ballot_sync(0xffffffffu, act);
+            const uint32_t below = ab & ((1u << lane) - 1u);
+            const int pl = below ? 31 - __clz(below) : lane;
+            const uint32_t pa = __shfl_sync(0xffffffffu, va[k], pl), pb = __shfl_sync(0xffffffffu, vb[k], pl);
+            act = act && !(below && pa == va[k] && pb == vb[k]);
+        }
 #endif
         const uint32_t bal = __ballot_sync(0xffffffffu, act);
         if (act) list[n + __popc(bal & ((1u << lane) - 1u))] = make_uint2(va[k], vb[k]);
