@@ -402,7 +402,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     // with the persistent grids capped so both fit on every SM.  Each chunk
     // has its own work region, so the chunks share nothing.
     const uint32_t tiles_per_frame = ((w + cclk::tile_w() - 1) / cclk::tile_w()) * ((h + cclk::tile_h() - 1) / cclk::tile_h());
-    const uint32_t min_chunk_tiles = uint32_t(env_int("CCL_PIPE_TILES", 16384));
+    const uint32_t min_chunk_tiles = uint32_t(env_int("CCL_PIPE_TILES", 24576));
     const uint32_t chunk = std::max(1u, (min_chunk_tiles + tiles_per_frame - 1) / tiles_per_frame);
     const bool pipe = env_int("CCL_PIPE", 1) != 0 && n >= 3 * chunk && !CCL_METRICS;
     if (!pipe) {
@@ -424,7 +424,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     ctx->last_split = false;
     CCL_CHECK(cudaEventRecord(ctx->ev[0], st));
     CCL_CHECK(cudaStreamWaitEvent(s2, ctx->ev[0], 0));  // inputs / previous work on the caller's stream
-    const int acap = env_int("CCL_PIPE_A", 7), ecap = env_int("CCL_PIPE_E", 3);  // tuned: scripts/batch_sweep.py
+    const int acap = env_int("CCL_PIPE_A", 8), ecap = env_int("CCL_PIPE_E", 3);  // tuned: scripts/batch_sweep.py
     for (uint32_t j = 0; j < nchunks; ++j) {
         const uint32_t f0 = j * chunk, nj = std::min(chunk, n - f0);
         cclk::LaunchArgs a{};
