@@ -667,15 +667,19 @@ __global__ void __launch_bounds__(C::NT, CCL_MINB)
         // already rewritten (parents always have smaller ids) end walks early.
         {
             volatile node_t* vP = P;
+            // two hops without branches (selects; most nodes are within two hops of
+            // their root after the jump round), a loop only for deeper chains
             for (uint32_t id = tid; id < nodes; id += C::NT) {
-                uint32_t p = vP[id];
-                if (!(p & kRoot)) {
+                const uint32_t p = vP[id];
+                const uint32_t q = (p & kRoot) ? p : uint32_t(vP[p & 0x7FFFu]);
+                uint32_t r = (q & kRoot) ? q : uint32_t(vP[q & 0x7FFFu]);
+                if (!(r & kRoot)) {
                     do {
                         mc.step();
-                        p = vP[p];
-                    } while (!(p & kRoot));
-                    vP[id] = node_t(p);
+                        r = vP[r];
+                    } while (!(r & kRoot));
                 }
+                if (!(p & kRoot)) vP[id] = node_t(r);
             }
         }
         const uint32_t nf = FR[0];
@@ -1151,15 +1155,19 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
         // ---- node table: every entry becomes its root's code
         {
             volatile node_t* vP = P;
+            // two hops without branches (selects; most nodes are within two hops of
+            // their root after the jump round), a loop only for deeper chains
             for (uint32_t id = tid; id < nodes; id += C::NT) {
-                uint32_t p = vP[id];
-                if (!(p & kRoot)) {
+                const uint32_t p = vP[id];
+                const uint32_t q = (p & kRoot) ? p : uint32_t(vP[p & 0x7FFFu]);
+                uint32_t r = (q & kRoot) ? q : uint32_t(vP[q & 0x7FFFu]);
+                if (!(r & kRoot)) {
                     do {
                         mc.step();
-                        p = vP[p];
-                    } while (!(p & kRoot));
-                    vP[id] = node_t(p);
+                        r = vP[r];
+                    } while (!(r & kRoot));
                 }
+                if (!(p & kRoot)) vP[id] = node_t(r);
             }
         }
         const uint32_t nf = FR[0];
