@@ -141,3 +141,22 @@ def test_errors(ccl):
         ccl.label_image(np.zeros((0, 5), np.uint8))
     with pytest.raises(ValueError):
         ccl.label_image(img, variant="bogus")
+
+
+def test_mixed_structures(ccl, oracle_mod):
+    """Tiles mixing vertically repeated run starts (vertical stripes, checkerboard
+    blocks: kernel (e)'s rotated run-start scatter, and tables staged in parts)
+    with random noise, so warps of one tile take different (e) paths; a dense
+    band exercises the union-list capacity of kernel (a)."""
+    rng = np.random.default_rng(11)
+    h, w = 1111, 1537
+    img = (rng.random((h, w)) < 0.5).astype(np.uint8)
+    img[:, 100:400] = (np.arange(300) % 2 == 0)[None, :]           # vertical stripes, period 2
+    yy, xx = np.mgrid[0:400, 0:300]
+    img[300:700, 500:800] = ((yy + xx) % 2 == 0)                      # checkerboard block
+    img[800:1000, :] = (rng.random((200, w)) < 0.85)                  # dense band
+    img[:, 1200:1203] = 1                                             # long vertical bars across tiles
+    want = oracle_mod.sequential_ccl(img)
+    for v in VARIANTS:
+        got = _gpu_label(ccl, img, v)
+        assert np.array_equal(got, want), f"{v}: {_first_diff(got, want)}"
