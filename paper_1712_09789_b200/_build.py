@@ -35,8 +35,16 @@ def _exp_defs() -> list[str]:
     return fl
 
 
+def _exp_xflags() -> list[str]:
+    """Experiment compiler flags (CCL_XFLAGS="-Xptxas,--allow-expensive-optimizations=true"); tagged as x<hash>."""
+    return [f for f in os.environ.get("CCL_XFLAGS", "").split(",") if f]
+
+
 def exp_tag() -> str:
     t = "_".join(f.replace("-DCCL_", "").replace("=", "").lower() for f in _exp_defs())
+    if _exp_xflags():
+        import hashlib
+        t += ("_" if t else "") + "x" + hashlib.sha1(",".join(_exp_xflags()).encode()).hexdigest()[:6]
     return t
 
 
@@ -67,7 +75,7 @@ def sources() -> list[str]:
 def _flags(extra: list[str] | None = None) -> list[str]:
     fl = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
                  "-I", os.path.join(REPO, "include"), "-I", CSRC]
-    fl += _exp_defs()
+    fl += _exp_defs() + _exp_xflags()
     return fl + (extra or [])
 
 
