@@ -23,8 +23,30 @@
 
 namespace cclk {
 
+// Programmatic dependent launch (as in ccl_kernels.cu): the small strip-seam
+// kernels are chained so that each one's launch overlaps its predecessor's
+// drain; every kernel waits for its predecessor before reading its output.
+__device__ __forceinline__ void aux_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void aux_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <class K, class... Args>
+static cudaError_t aux_launch_pdl(K kernel, unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = CCL_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ------------------------------------------------------------ strip export
 __global__ void k_strip_roots(const uint32_t* se, Forest fst, uint32_t* L, Geo g, uint32_t* out, uint32_t* croot) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * g.W) return;
     const bool top = i < g.W;
@@ -45,6 +67,8 @@ __global__ void k_strip_roots(const uint32_t* se, Forest fst, uint32_t* L, Geo g
 // carrying the root is found with an atomicMin on the root's scratch entry in
 // L, encoded as base + x (< base + W <= root, so the root value itself loses).
 __global__ void k_strip_repmin(uint32_t* L, Geo g, const uint32_t* out) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
     const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= g.W) return;
     const uint32_t r = out[g.W + x];
@@ -55,6 +79,8 @@ __global__ void k_strip_repmin(uint32_t* L, Geo g, const uint32_t* out) {
 }
 
 __global__ void k_strip_reps(const uint32_t* L, Geo g, uint32_t k, uint32_t* out) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * g.W) return;
     const uint32_t r = out[i];
@@ -87,7 +113,17 @@ __device__ __forceinline__ uint32_t seam_find(uint32_t* par, uint32_t j) {
     }
     return j;
 }
+__global__ void k_seam_init(const uint32_t* all, uint32_t N, uint32_t W, uint32_t* par) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(N) * 2 * W) return;
+    const uint32_t s = uint32_t(t / (2 * W)), i = uint32_t(t - uint64_t(s) * 2 * W);
+    par[t] = all[size_t(s) * 4 * W + 2 * W + i];  // every node starts at its exported representative
+}
 __global__ void k_seam_union(const uint32_t* all, uint32_t N, uint32_t W, uint32_t* par) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= uint64_t(N - 1) * W) return;
     const uint32_t s = uint32_t(t / W), x = uint32_t(t - uint64_t(s) * W);
@@ -110,13 +146,14 @@ __global__ void k_seam_union(const uint32_t* all, uint32_t N, uint32_t W, uint32
 }
 __global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const uint32_t* par, const uint32_t* croot,
                              Forest fst) {
+    aux_pdl_wait();
+    aux_pdl_trigger();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * W) return;
     const uint32_t j = k * 2 * W + i;
     const uint32_t r = seam_key(all, W, j);
     if (r == kBG) return;
-    uint32_t q = j;
-    while (par[q] != q) q = par[q];
+    const uint32_t q = seam_find(const_cast<uint32_t*>(par), j);  // path halving: all unions are done
     fst.f[2 * size_t(croot[i]) + 1] = seam_key(all, W, q);  // final label of this strip root
 }
 
@@ -124,26 +161,29 @@ cudaError_t launch_strip_export(const Geo& g, uint32_t* labels, uint32_t* work, 
                                 cudaStream_t s) {
     const unsigned nb2 = (2 * g.W + 255) / 256, nb1 = (g.W + 255) / 256;
     uint32_t* se = strip_area_ptr(work, g);
-    k_strip_roots<<<nb2, 256, 0, s>>>(se, Forest{forest_ptr(work, g)}, labels, g, seam_out, se + 2 * size_t(g.W));
-    k_strip_repmin<<<nb1, 256, 0, s>>>(labels, g, seam_out);
-    k_strip_reps<<<nb2, 256, 0, s>>>(labels, g, k, seam_out);
-    return cudaGetLastError();
+    cudaError_t e = aux_launch_pdl(k_strip_roots, nb2, 256, s, static_cast<const uint32_t*>(se),
+                                   Forest{forest_ptr(work, g)}, labels, g, seam_out, se + 2 * size_t(g.W));
+    if (e == cudaSuccess) e = aux_launch_pdl(k_strip_repmin, nb1, 256, s, labels, g, static_cast<const uint32_t*>(seam_out));
+    if (e == cudaSuccess)
+        e = aux_launch_pdl(k_strip_reps, nb2, 256, s, static_cast<const uint32_t*>(labels), g, k, seam_out);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* all, uint32_t N, uint32_t k, uint32_t* labels,
                                  uint32_t* work, uint32_t* scratch, cudaStream_t s) {
     (void)labels;
     const size_t W = g.W;
-    cudaError_t e = cudaMemcpy2DAsync(scratch, 2 * W * 4, all + 2 * W, 4 * W * 4, 2 * W * 4, N,
-                                      cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return e;
-    if (N > 1) {
+    cudaError_t e = aux_launch_pdl(k_seam_init, unsigned((uint64_t(N) * 2 * W + 255) / 256), 256, s, all, N, g.W,
+                                   scratch);
+    if (e == cudaSuccess && N > 1) {
         const uint64_t n = uint64_t(N - 1) * W;
-        k_seam_union<<<unsigned((n + 255) / 256), 256, 0, s>>>(all, N, g.W, scratch);
+        e = aux_launch_pdl(k_seam_union, unsigned((n + 255) / 256), 256, s, all, N, g.W, scratch);
     }
-    k_seam_apply<<<unsigned((2 * W + 255) / 256), 256, 0, s>>>(all, g.W, k, scratch,
-                                                              strip_area_ptr(work, g) + 2 * W, Forest{forest_ptr(work, g)});
-    return cudaGetLastError();
+    if (e == cudaSuccess)
+        e = aux_launch_pdl(k_seam_apply, unsigned((2 * W + 255) / 256), 256, s, all, g.W, k,
+                           static_cast<const uint32_t*>(scratch), static_cast<const uint32_t*>(strip_area_ptr(work, g) + 2 * W),
+                           Forest{forest_ptr(work, g)});
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ------------------------------------------------------------ compaction
