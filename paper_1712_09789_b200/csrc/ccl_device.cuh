@@ -20,7 +20,7 @@
 #define CCL_METRICS 0
 #endif
 #ifndef CCL_UNITE_COMPRESS
-#define CCL_UNITE_COMPRESS 1  // kernel (d): both start nodes of a union point at the root afterwards
+#define CCL_UNITE_COMPRESS 2  // kernel (d): after a union both start nodes (and the node above each, when not already one hop below) point at the root
 #endif
 
 namespace cclk {
@@ -165,9 +165,19 @@ struct Forest {
         const uint32_t a0 = a, b0 = b;
         // afterwards both start nodes point at the class root they reached: a
         // tile's seam root meets many seams, and these are its own (cold) lines
+#if CCL_UNITE_COMPRESS >= 2
+        // ... and so does the first node above each start when it is not one
+        // hop below the root already (written once per node and change: a node
+        // that points at the root is never rewritten, so hot nodes stay cold)
+        uint32_t a1 = 0xFFFFFFFFu, a1p = 0, b1 = 0xFFFFFFFFu, b1p = 0;
+#endif
         auto done = [&](uint32_t r) {
             if (a0 != r && a0 != a) f[2 * size_t(a0)] = r;
             if (b0 != r && b0 != b) f[2 * size_t(b0)] = r;
+#if CCL_UNITE_COMPRESS >= 2
+            if (a1 != 0xFFFFFFFFu && a1 != r && a1p != r) f[2 * size_t(a1)] = r;
+            if (b1 != 0xFFFFFFFFu && b1 != r && b1p != r) f[2 * size_t(b1)] = r;
+#endif
         };
 #else
         auto done = [](uint32_t) {};
@@ -179,6 +189,10 @@ struct Forest {
                 uint2 An = A, Bn = B;
                 if (ca) An = node(A.x);
                 if (cb) Bn = node(B.x);
+#if CCL_UNITE_COMPRESS >= 2
+                if (ca && a1 == 0xFFFFFFFFu) { a1 = A.x; a1p = An.x; }
+                if (cb && b1 == 0xFFFFFFFFu) { b1 = B.x; b1p = Bn.x; }
+#endif
                 // (no path halving here: at high density every union climbs
                 // through the same few hot nodes and the extra stores thrash)
                 m.step(uint32_t(ca) + uint32_t(cb));
