@@ -336,9 +336,65 @@ def measure_configs(ccl, timer, ctx, dev, stream, steps=5, warmup=3, cpu=True):
     torch.cuda.empty_cache()
     big = ccl.random_image_device(32768, 32768, 0.5, 0, device=dev.index)
     out["5_single32768"] = one(big, 32768, 32768)
+    out["5_strip_rank_model"] = strip_rank_model(ccl, big, dev, stream, ctx)
     del big
     torch.cuda.empty_cache()
     return out
+
+
+def strip_rank_model(ccl, img, dev, stream, ctx, ns=(2, 4, 8), reps=4):
+    """Config 5 on ONE GPU as a per-rank cost model: for N strips, the kernels
+    rank N/2 runs in a multi-GPU step -- (a)+(d) on its 32768/N rows, the seam
+    export, the seam union-find over all N exports, (d2)+(e) -- timed back to
+    back with CUDA events (every other strip's export prepared first).  The
+    NVLink exchange of N x 16 W bytes is not included (one GPU here).
+    `projected_gpx_s` = 32768^2 / rank step: the strong-scaling curve the
+    multi-GPU run should approach (scripts/strip_model.py prints the phases)."""
+    import torch
+    from paper_1712_09789_b200 import _lib, _check
+    from paper_1712_09789_b200.strips import split_rows
+    H, W = img.shape
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    out = torch.empty((H, W), dtype=torch.uint32, device=dev)
+    res = {}
+    for n in ns:
+        parts = split_rows(H, n)
+        seams = torch.empty((n, 4 * W), dtype=torch.int32, device=dev)
+        scratch = torch.empty(int(_lib.ccl_strip_scratch_words(n, W)), dtype=torch.int32, device=dev)
+        works = [torch.zeros(int(_lib.ccl_work_bytes(W, h, 1)), dtype=torch.uint8, device=dev) for _, h in parts]
+        k = n // 2
+
+        def phase1(j):
+            r0, h = parts[j]
+            im, lo = img[r0:r0 + h], out[r0:r0 + h]
+            _check(_lib.ccl_strip_local(ctx.handle, im.data_ptr(), im.stride(0), W, h, r0, H, lo.data_ptr(),
+                                        works[j].data_ptr(), 0, s))
+            _check(_lib.ccl_strip_seam_export(ctx.handle, W, h, r0, H, j, lo.data_ptr(), works[j].data_ptr(),
+                                              seams[j].data_ptr(), s))
+
+        for j in range(n):
+            phase1(j)
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.ExternalStream(s) if stream is None else stream)
+            phase1(k)
+            r0, h = parts[k]
+            lo = out[r0:r0 + h]
+            _check(_lib.ccl_strip_seam_resolve(ctx.handle, seams.data_ptr(), n, k, W, h, r0, H, lo.data_ptr(),
+                                               works[k].data_ptr(), scratch.data_ptr(), s))
+            _check(_lib.ccl_strip_final(ctx.handle, W, h, r0, H, lo.data_ptr(), works[k].data_ptr(), 0, s))
+            e1.record(torch.cuda.ExternalStream(s) if stream is None else stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[len(ts) // 2]
+        res[f"N{n}"] = {"rank_ms": ms, "projected_gpx_s": H * W / (ms * 1e-3) / 1e9, "rows_per_rank": parts[k][1]}
+        del seams, scratch, works
+    res["note"] = ("per-rank kernels of the N-GPU step measured on one GPU (L2 warm between phases, no flush); "
+                   "the NVLink seam exchange (N x 16 W bytes) is not included")
+    torch.cuda.empty_cache()
+    return res
 
 
 def batch_point(ccl, timer, ctx, dev, stream, nframes, first=0, steps=3, warmup=2):
