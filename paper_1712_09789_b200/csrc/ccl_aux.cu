@@ -4,8 +4,10 @@
 // space with kernels (a)-(d); then a seam step merges components across the
 // horizontal strip boundaries:
 //   export  : k_strip_roots -> k_strip_repmin -> k_strip_reps
-//   exchange: all-gather of every strip's 4*W seam words (caller: NCCL)
-//   resolve : k_seam_union (identical on every strip) -> k_seam_apply
+//   exchange: every strip's 4*W seam words into every rank's exchange area
+//             (ccl_strips.cu strip groups; a device-local copy for virtual strips)
+//   resolve : k_seam_init -> k_seam_union (identical on every strip) -> k_seam_apply
+// (all six PDL-chained: each waits for its predecessor before reading)
 // Kernel (a) leaves, in the strip area of the work buffer, the compact forest
 // node of every top/bottom-row pixel; k_strip_roots resolves them to the
 // strip-local roots (exported by key = global raster index) and remembers the
@@ -144,7 +146,7 @@ __global__ void k_seam_union(const uint32_t* all, uint32_t N, uint32_t W, uint32
         if (atomicCAS(par + b, b, a) == b) return;  // link larger-key root below smaller-key root
     }
 }
-__global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const uint32_t* par, const uint32_t* croot,
+__global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, uint32_t* par, const uint32_t* croot,
                              Forest fst) {
     aux_pdl_wait();
     aux_pdl_trigger();
@@ -153,7 +155,7 @@ __global__ void k_seam_apply(const uint32_t* all, uint32_t W, uint32_t k, const 
     const uint32_t j = k * 2 * W + i;
     const uint32_t r = seam_key(all, W, j);
     if (r == kBG) return;
-    const uint32_t q = seam_find(const_cast<uint32_t*>(par), j);  // path halving: all unions are done
+    const uint32_t q = seam_find(par, j);  // path halving: all unions are done
     fst.f[2 * size_t(croot[i]) + 1] = seam_key(all, W, q);  // final label of this strip root
 }
 
@@ -181,7 +183,7 @@ cudaError_t launch_strip_resolve(const Geo& g, const uint32_t* all, uint32_t N, 
     }
     if (e == cudaSuccess)
         e = aux_launch_pdl(k_seam_apply, unsigned((2 * W + 255) / 256), 256, s, all, g.W, k,
-                           static_cast<const uint32_t*>(scratch), static_cast<const uint32_t*>(strip_area_ptr(work, g) + 2 * W),
+                           scratch, static_cast<const uint32_t*>(strip_area_ptr(work, g) + 2 * W),
                            Forest{forest_ptr(work, g)});
     return e != cudaSuccess ? e : cudaGetLastError();
 }
