@@ -999,8 +999,8 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
             {   // linked runs: one trip per first overlap (the run holding it
                 // links to the band run above holding it); roots: one trip per
-                // run without an overlap, coded by its first top-row pixel or,
-                // without one, by its first column in the bottom row
+                // run without an overlap, coded by its first top-row pixel (first
+                // loop) or, without one, by its first column in the bottom row
                 uint32_t ff = firstm;
                 while (ff) {
                     const uint32_t f = lowbit(ff);
@@ -1008,12 +1008,19 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                     P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
                 }
                 const uint32_t top_root = tfirst & ~seg_back(firstm, bs[k]);  // first top pixels of unlinked runs
-                uint32_t rr = top_root | (bs[k] & ~seg_back(tfirst, bs[k]));  // ... and starts of runs without one
-                while (rr) {
-                    const uint32_t a = lowbit(rr);
-                    rr &= rr - 1;
-                    const uint32_t pos = (((top_root >> a) & 1u) ? rowpos0 : rowpos1) + a;
-                    P[node_of(pfx[k], bs[k], a)] = node_t(kRoot | pos);
+                {   // two loops with a constant row base each (no per-root row select)
+                    uint32_t rt = top_root, rb = bs[k] & ~seg_back(tfirst, bs[k]);
+                    const uint32_t c0 = kRoot | rowpos0, c1 = kRoot | rowpos1;
+                    while (rt) {
+                        const uint32_t a = lowbit(rt);
+                        rt &= rt - 1;
+                        P[node_of(pfx[k], bs[k], a)] = node_t(c0 + a);
+                    }
+                    while (rb) {
+                        const uint32_t a = lowbit(rb);
+                        rb &= rb - 1;
+                        P[node_of(pfx[k], bs[k], a)] = node_t(c1 + a);
+                    }
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
