@@ -184,6 +184,24 @@ __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x, Ctr& m) {
     }
     return x;
 }
+// nfind that also hands back the root's entry (its code): no re-read by the caller
+__device__ __forceinline__ uint32_t nfind_code(node_t* P, uint32_t x, uint32_t& code, Ctr& m) {
+    volatile node_t* vP = P;
+    uint32_t p = vP[x];
+    while (!(p & kRoot)) {
+        m.step();
+        const uint32_t gp = vP[p];
+        if (gp & kRoot) {
+            code = gp;
+            return p;
+        }
+        vP[x] = node_t(gp);  // path halving (ancestor only)
+        x = gp;
+        p = vP[x];
+    }
+    code = p;
+    return x;
+}
 __device__ __forceinline__ void nunion(node_t* P, uint32_t a, uint32_t b, Ctr& m) {
     volatile node_t* vP = P;
     for (;;) {
@@ -787,13 +805,11 @@ __device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, 
 // Min-union on root codes (positions): the root whose code is larger is
 // linked below the other with a CAS on its entry.
 __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b, Ctr& m) {
-    volatile node_t* vP = P;
     for (;;) {
-        a = nfind(P, a, m);
-        b = nfind(P, b, m);
+        uint32_t ca, cb;
+        a = nfind_code(P, a, ca, m);
+        b = nfind_code(P, b, cb, m);
         if (a == b) return;
-        uint32_t ca = vP[a], cb = vP[b];
-        if (!(ca & kRoot) || !(cb & kRoot)) continue;  // linked meanwhile: find again
         if ((ca & kCode) < (cb & kCode)) {
             const uint32_t t = a; a = b; b = t;
             const uint32_t tc = ca; ca = cb; cb = tc;
