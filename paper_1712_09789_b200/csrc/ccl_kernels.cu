@@ -883,7 +883,6 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             mbar_wait(bar, it & 1u);
             constexpr int CPR = C::TW / 16;
             uint16_t* M16 = reinterpret_cast<uint16_t*>(M);
-#pragma unroll
             static_assert((C::TH * CPR) % C::NT == 0, "whole mask-build rounds");
             constexpr int KK = C::TH * CPR / C::NT;
             uint4 q[KK];
