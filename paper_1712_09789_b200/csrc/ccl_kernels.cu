@@ -764,37 +764,26 @@ __device__ __forceinline__ uint32_t band_starts(uint32_t t, uint32_t u, uint32_t
     const uint32_t cl = (((tl >> 31) & t) | ((ul >> 31) & u)) & 1u;  // bit 0 linked to the word on the left
     return (t | u) & ~((lk << 1) | cl);
 }
-// First set bit of x in every segment of a word, segments starting at the bits
-// of `starts` (a segmented prefix-OR by doubling: bit p may look back k bits
-// while no segment starts in (p-k, p]).
+// Segments of a word start at the bits of `starts` and run up to the next
+// start.  seg_first: the first set bit of x in every segment (bits below the
+// first start belong to the word on the left and yield none).  A carry
+// injected at every start runs through the zeros of x and stops at the
+// segment's first set bit; the bit before each start is forced to 0 in ~x, so
+// no carry crosses into the next segment.
 __device__ __forceinline__ uint32_t seg_first(uint32_t x, uint32_t starts) {
-    const uint32_t can = ~starts;
-    uint32_t inc = x, c = can;
-    inc |= (inc << 1) & c;
-    c &= c << 1;
-    inc |= (inc << 2) & c;
-    c &= c << 2;
-    inc |= (inc << 4) & c;
-    c &= c << 4;
-    inc |= (inc << 8) & c;
-    c &= c << 8;
-    inc |= (inc << 16) & c;
-    return x & ~((inc << 1) & can);
+    return x & ((~x & ~(starts >> 1)) + starts);
 }
-// Bits of every segment (as in seg_first) that hold a set bit of x at or after them.
-__device__ __forceinline__ uint32_t seg_back(uint32_t x, uint32_t starts) {
-    const uint32_t can = ~(starts >> 1);  // bit p may look at p + 1
-    uint32_t inc = x, c = can;
-    inc |= (inc >> 1) & c;
-    c &= c >> 1;
-    inc |= (inc >> 2) & c;
-    c &= c >> 2;
-    inc |= (inc >> 4) & c;
-    c &= c >> 4;
-    inc |= (inc >> 8) & c;
-    c &= c >> 8;
-    inc |= (inc >> 16) & c;
-    return inc;
+// seg_back: the bits of every segment that hold a set bit of x at or after
+// them (the region below the first start is a segment too).  On the
+// bit-reversed word this is a segmented prefix-OR: the bits before a segment's
+// first set bit are the carry chain of the same addition (carry-in bits
+// shifted down), and an empty segment's chain ends on its last bit.  rs =
+// (brev(starts) << 1) | 1 and re = brev(starts) | bit 31: segment starts and
+// ends of the reversed word (shared by every scan over the same starts).
+__device__ __forceinline__ uint32_t seg_back(uint32_t x, uint32_t rs, uint32_t re) {
+    const uint32_t xr = __brev(x), y = ~xr & ~re, r = y + rs;
+    const uint32_t chain = (r ^ y ^ rs) >> 1, emp = r & ~xr & re;
+    return __brev(~(chain | emp));
 }
 template <class C>
 __device__ __forceinline__ uint32_t band_starts_at(const uint32_t* M, int band, int w) {
@@ -1007,11 +996,11 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
             const uint32_t os = (o & ~(o << 1)) & ~ocont;
             const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
-            // the part of the word before its first band start belongs to a band
-            // run of the word on the left (that lane owns the node)
-            const uint32_t contp = bs[k] ? (1u << (lowbit(bs[k]))) - 1u : 0xFFFFFFFFu;
-            const uint32_t firstm = seg_first(o, bs[k]) & ~contp;   // first overlap of each band run
-            const uint32_t tfirst = seg_first(tm[k], bs[k]) & ~contp;  // first top-row pixel of each band run
+            // (seg_first yields nothing below the word's first band start: that
+            // part belongs to a band run of the word on the left, whose lane owns the node)
+            const uint32_t firstm = seg_first(o, bs[k]);      // first overlap of each band run
+            const uint32_t tfirst = seg_first(tm[k], bs[k]);  // first top-row pixel of each band run
+            const uint32_t rbs = __brev(bs[k]), rss = (rbs << 1) | 1u, rse = rbs | 0x80000000u;
             {   // linked runs: one trip per first overlap (the run holding it
                 // links to the band run above holding it); roots: one trip per
                 // run without an overlap, coded by its first top-row pixel (first
@@ -1022,9 +1011,9 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                     ff &= ff - 1;
                     P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
                 }
-                const uint32_t top_root = tfirst & ~seg_back(firstm, bs[k]);  // first top pixels of unlinked runs
+                const uint32_t top_root = tfirst & ~seg_back(firstm, rss, rse);  // first top pixels of unlinked runs
                 {   // two loops with a constant row base each (no per-root row select)
-                    uint32_t rt = top_root, rb = bs[k] & ~seg_back(tfirst, bs[k]);
+                    uint32_t rt = top_root, rb = bs[k] & ~seg_back(tfirst, rss, rse);
                     const uint32_t c0 = kRoot | rowpos0, c1 = kRoot | rowpos1;
                     while (rt) {
                         const uint32_t a = lowbit(rt);
