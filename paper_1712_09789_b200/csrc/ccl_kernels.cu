@@ -241,15 +241,18 @@ __device__ __forceinline__ void metrics_phase(const Geo& g, int k, Ctr& m) {
 #endif
 }
 
-// Dynamic shared memory rounded up to 1024 B (128B-swizzled TMA tiles).  The
-// offset is added to the __shared__ array itself (no integer round trip), so
-// the compiler keeps the shared address space: LDS/STS with 32-bit addresses
-// instead of generic 64-bit LD/ST.
+// Dynamic shared memory rounded up to ALIGN bytes (1024 B: 128B-swizzled TMA
+// tiles).  The base is rounded as a 32-bit shared address, passed through an
+// empty asm and converted back: the compiler still sees a shared pointer
+// (LDS/STS with 32-bit addresses, not generic LD/ST) but can no longer
+// re-derive the base from SR_CgaCtaId inside every loop (4 instructions per
+// trip under kernel (a)'s register cap); it keeps it in a uniform register.
 template <uint32_t ALIGN = 1024>
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t off = (ALIGN - (smem_u32(smem_raw) & (ALIGN - 1))) & (ALIGN - 1);
-    return smem_raw + off;
+    uint32_t a = (smem_u32(smem_raw) + (ALIGN - 1)) & ~(ALIGN - 1);
+    asm volatile("" : "+r"(a));
+    return static_cast<uint8_t*>(__cvta_shared_to_generic(a));
 }
 
 // Work-buffer view of one tile (tile index tg over frames x tile rows x tile cols).
