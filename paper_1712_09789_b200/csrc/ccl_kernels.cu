@@ -998,36 +998,30 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t o = tm[k] & ua[k];
             const uint32_t ocont = (o & 1u) & ((tl & ual) >> 31);  // overlap continuing from the left word
             const uint32_t os = (o & ~(o << 1)) & ~ocont;
-            const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc), rowpos1 = uint32_t(r1 * C::TW + 32 * wc);
+            const uint32_t rowpos0 = uint32_t(r0 * C::TW + 32 * wc);  // the bottom row's: + TW
             // (seg_first yields nothing below the word's first band start: that
             // part belongs to a band run of the word on the left, whose lane owns the node)
             const uint32_t firstm = seg_first(o, bs[k]);      // first overlap of each band run
             const uint32_t tfirst = seg_first(tm[k], bs[k]);  // first top-row pixel of each band run
             const uint32_t rbs = __brev(bs[k]), rss = (rbs << 1) | 1u, rse = rbs | 0x80000000u;
-            {   // linked runs: one trip per first overlap (the run holding it
-                // links to the band run above holding it); roots: one trip per
-                // run without an overlap, coded by its first top-row pixel (first
-                // loop) or, without one, by its first column in the bottom row
-                uint32_t ff = firstm;
-                while (ff) {
-                    const uint32_t f = lowbit(ff);
-                    ff &= ff - 1;
-                    P[node_of(pfx[k], bs[k], f)] = node_t(node_of(upfx[k], ubs[k], f));
-                }
-                const uint32_t top_root = tfirst & ~seg_back(firstm, rss, rse);  // first top pixels of unlinked runs
-                {   // two loops with a constant row base each (no per-root row select)
-                    uint32_t rt = top_root, rb = bs[k] & ~seg_back(tfirst, rss, rse);
-                    const uint32_t c0 = kRoot | rowpos0, c1 = kRoot | rowpos1;
-                    while (rt) {
-                        const uint32_t a = lowbit(rt);
-                        rt &= rt - 1;
-                        P[node_of(pfx[k], bs[k], a)] = node_t(c0 + a);
-                    }
-                    while (rb) {
-                        const uint32_t a = lowbit(rb);
-                        rb &= rb - 1;
-                        P[node_of(pfx[k], bs[k], a)] = node_t(c1 + a);
-                    }
+            {   // one marker bit per band run, in run order: its first overlap
+                // (the run links to the band run above holding it), else its first
+                // top-row pixel (a root, coded by it), else its start (a root
+                // without a top-row pixel here, coded by its first bottom
+                // column); the i-th marker is node pfx + i, so one loop whose
+                // trip count is the lane's run count (not the sum of three
+                // per-loop warp maxima) and no rank popcount for the node
+                const uint32_t top_root = tfirst & ~seg_back(firstm, rss, rse);
+                const uint32_t rb = bs[k] & ~seg_back(tfirst, rss, rse);
+                uint32_t mk = firstm | top_root | rb;
+                const uint32_t c0 = kRoot | rowpos0;
+                node_t* dst = P + pfx[k];
+                while (mk) {
+                    const uint32_t lb = mk & (0u - mk);
+                    const uint32_t a = 31u - __clz(lb);
+                    mk ^= lb;
+                    const uint32_t code = c0 + a + ((rb & lb) ? uint32_t(C::TW) : 0u);
+                    *dst++ = node_t((firstm & lb) ? node_of(upfx[k], ubs[k], a) : code);
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
