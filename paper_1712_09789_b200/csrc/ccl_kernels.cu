@@ -990,6 +990,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
         // above that holds its first overlap in its word (plain stores); a root
         // band run carries its minimum pixel as its code
         uint32_t U[WPL];
+        uint32_t nlink = 0;  // this lane's linked runs
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             const int wc = wc0 + k;
@@ -1043,6 +1044,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 }
             }
             U[k] = os & ~firstm;  // remaining overlaps
+            nlink += __popc(firstm);
         }
         // remaining overlaps -> this warp's union list
         uint32_t* UL = reinterpret_cast<uint32_t*>(smem + A::UL_OFF) + warp * A::UL_CAP;
@@ -1071,13 +1073,17 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 }
             }
         }
-        __syncthreads();
+        // the jump round pays where chains form: tiles where most lanes link
+        // at least a third of their runs (lanes without runs count as linking);
+        // sparse tiles and tiles of isolated runs (checkerboards) skip it
+        // (output-invariant either way: a jump only shortens a path)
+        const bool do_jump = __syncthreads_count(3u * nlink >= cnt) > C::NT / 2;
         CCL_PH(10);
 
         // ---- one pointer-jump round (no barrier after it: jumps and unions only
         // replace an entry by an ancestor, unions CAS root entries only)
 #pragma unroll 1
-        for (int j = 0; j < CCL_BJUMP; ++j) {
+        for (int j = 0; j < (do_jump ? CCL_BJUMP : 0); ++j) {
             volatile node_t* vP = P;
             for (uint32_t id = tid; id < nodes; id += C::NT) {
                 const uint32_t p = vP[id];
