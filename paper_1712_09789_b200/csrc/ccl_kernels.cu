@@ -185,19 +185,26 @@ __device__ __forceinline__ uint32_t nfind(node_t* P, uint32_t x, Ctr& m) {
     return x;
 }
 // nfind that also hands back the root's entry (its code): no re-read by the caller
+// Band kernel node HANDLES: a node's handle is its id << kNS = the byte offset
+// of its entry in the table, so a parent entry addresses its parent's entry
+// directly (LDS [handle + base], no index arithmetic per hop of a walk).
+// Handles stay below 0x2000 (4096 nodes), clear of the kRoot / kSeam code bits.
+constexpr uint32_t kNS = 1u;
+__device__ __forceinline__ volatile node_t* nslot(node_t* P, uint32_t h) {
+    return reinterpret_cast<volatile node_t*>(reinterpret_cast<char*>(P) + h);
+}
 __device__ __forceinline__ uint32_t nfind_code(node_t* P, uint32_t x, uint32_t& code, Ctr& m) {
-    volatile node_t* vP = P;
-    uint32_t p = vP[x];
+    uint32_t p = *nslot(P, x);
     while (!(p & kRoot)) {
         m.step();
-        const uint32_t gp = vP[p];
+        const uint32_t gp = *nslot(P, p);
         if (gp & kRoot) {
             code = gp;
             return p;
         }
-        vP[x] = node_t(gp);  // path halving (ancestor only)
+        *nslot(P, x) = node_t(gp);  // path halving (ancestor only)
         x = gp;
-        p = vP[x];
+        p = *nslot(P, x);
     }
     code = p;
     return x;
@@ -807,7 +814,7 @@ __device__ __forceinline__ void nunion_pos(node_t* P, uint32_t a, uint32_t b, Ct
             const uint32_t tc = ca; ca = cb; cb = tc;
         }
         m.cas();
-        if (atomicCAS(reinterpret_cast<unsigned short*>(P + a), static_cast<unsigned short>(ca),
+        if (atomicCAS(const_cast<unsigned short*>(reinterpret_cast<volatile unsigned short*>(nslot(P, a))), static_cast<unsigned short>(ca),
                       static_cast<unsigned short>(b)) == ca)
             return;
     }
@@ -945,14 +952,14 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t u1 = __shfl_sync(0xffffffffu, um[0], 31), s1 = __shfl_sync(0xffffffffu, bs[0], 31);
             const uint32_t p1 = __shfl_sync(0xffffffffu, pfx[0], 31);
             const int c = 32 * wc0 + lane;
-            BN[c] = ((t0 >> lane) & 1u) ? uint16_t(node_of(p0, s0, lane)) : uint16_t(0xFFFFu);
-            BN[C::TW + c] = ((u1 >> lane) & 1u) ? uint16_t(node_of(p1, s1, lane)) : uint16_t(0xFFFFu);
+            BN[c] = ((t0 >> lane) & 1u) ? uint16_t(node_of(p0, s0, lane) << kNS) : uint16_t(0xFFFFu);
+            BN[C::TW + c] = ((u1 >> lane) & 1u) ? uint16_t(node_of(p1, s1, lane) << kNS) : uint16_t(0xFFFFu);
             if (wc0 == 0) {  // column 0 starts a band run
-                BN[2 * C::TW + r0] = (tm[0] & 1u) ? uint16_t(pfx[0]) : uint16_t(0xFFFFu);
-                BN[2 * C::TW + r1] = (um[0] & 1u) ? uint16_t(pfx[0]) : uint16_t(0xFFFFu);
+                BN[2 * C::TW + r0] = (tm[0] & 1u) ? uint16_t(pfx[0] << kNS) : uint16_t(0xFFFFu);
+                BN[2 * C::TW + r1] = (um[0] & 1u) ? uint16_t(pfx[0] << kNS) : uint16_t(0xFFFFu);
             }
             if (wc0 == WPR - 1) {  // column TW-1 is in the word's last band run
-                const uint16_t last = uint16_t(pfx[0] + __popc(bs[0]) - 1u);
+                const uint16_t last = uint16_t((pfx[0] + __popc(bs[0]) - 1u) << kNS);
                 BN[2 * C::TW + C::TH + r0] = (tm[0] >> 31) ? last : uint16_t(0xFFFFu);
                 BN[2 * C::TW + C::TH + r1] = (um[0] >> 31) ? last : uint16_t(0xFFFFu);
             }
@@ -1022,7 +1029,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                     const uint32_t a = 31u - __clz(lb);
                     mk ^= lb;
                     const uint32_t code = c0 + a + ((rb & lb) ? uint32_t(C::TW) : 0u);
-                    *dst++ = node_t((firstm & lb) ? node_of(upfx[k], ubs[k], a) : code);
+                    *dst++ = node_t((firstm & lb) ? node_of(upfx[k], ubs[k], a) << kNS : code);
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
@@ -1068,7 +1075,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                     while (U[k]) {
                         const uint32_t b = lowbit(U[k]);
                         U[k] &= U[k] - 1;
-                        *dst++ = node_of(pfx[k], bs[k], b) | (node_of(upfx[k], ubs[k], b) << 16);
+                        *dst++ = (node_of(pfx[k], bs[k], b) << kNS) | (node_of(upfx[k], ubs[k], b) << (16 + kNS));
                     }
                 }
             }
@@ -1084,12 +1091,11 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
         // replace an entry by an ancestor, unions CAS root entries only)
 #pragma unroll 1
         for (int j = 0; j < (do_jump ? CCL_BJUMP : 0); ++j) {
-            volatile node_t* vP = P;
-            for (uint32_t id = tid; id < nodes; id += C::NT) {
-                const uint32_t p = vP[id];
-                const uint32_t pp = (p & kRoot) ? p : vP[p];
+            for (uint32_t h = uint32_t(tid) << kNS; h < (nodes << kNS); h += uint32_t(C::NT) << kNS) {
+                const uint32_t p = *nslot(P, h);
+                const uint32_t pp = (p & kRoot) ? p : uint32_t(*nslot(P, p));
                 if (!(p & kRoot)) mc.step();
-                if (!(pp & kRoot)) vP[id] = node_t(pp);
+                if (!(pp & kRoot)) *nslot(P, h) = node_t(pp);
             }
             if (j + 1 < CCL_BJUMP) __syncthreads();
         }
@@ -1103,7 +1109,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             while (U[k]) {  // pairs that did not fit in the list
                 const uint32_t b = lowbit(U[k]);
                 U[k] &= U[k] - 1;
-                nunion_pos(P, node_of(pfx[k], bs[k], b), node_of(upfx[k], ubs[k], b), mc);
+                nunion_pos(P, node_of(pfx[k], bs[k], b) << kNS, node_of(upfx[k], ubs[k], b) << kNS, mc);
             }
         }
         __syncthreads();
@@ -1115,21 +1121,21 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
         const bool has_bot = ty + 1 < g.nty || g.edge_below;
         const bool has_left = tx > 0, has_right = tx + 1 < g.ntx;
         static_assert(C::NT == C::TW && C::NT == 2 * C::TH, "one top, one bottom and one side item per thread");
-        auto mark = [&](uint32_t x) {  // x: the node of a foreground pixel on a facing side
-            uint32_t p = P[x];
+        auto mark = [&](uint32_t x) {  // x: the node (handle) of a foreground pixel on a facing side
+            uint32_t p = *nslot(P, x);
             while (!(p & kRoot)) {
                 mc.step();
                 x = p;
-                p = P[x];
+                p = *nslot(P, x);
             }
-            const uint32_t bit = 1u << (x & 31);
-            if (!(atomicOr(&FB[x >> 5], bit) & bit)) {
+            const uint32_t id = x >> kNS, bit = 1u << (id & 31);
+            if (!(atomicOr(&FB[id >> 5], bit) & bit)) {
                 const uint32_t k = atomicAdd(FR, 1u);
                 const uint32_t n = t * uint32_t(C::MAXF) + k;
                 fst.f[2 * size_t(n)] = n;
                 fst.f[2 * size_t(n) + 1] = pos_gidx<C>(p & kCode, x0, y0, g);
                 FR[1 + k] = n;
-                P[x] = node_t(kRoot | kSeam | k);
+                *nslot(P, x) = node_t(kRoot | kSeam | k);
             }
         };
         {   // one item per RUN of foreground pixels along a facing side (the run's
@@ -1171,17 +1177,18 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             volatile node_t* vP = P;
             // two hops without branches (selects; most nodes are within two hops of
             // their root after the jump round), a loop only for deeper chains
-            for (uint32_t id = tid; id < nodes; id += C::NT) {
-                const uint32_t p = vP[id];
-                const uint32_t q = (p & kRoot) ? p : uint32_t(vP[p & 0x7FFFu]);
-                uint32_t r = (q & kRoot) ? q : uint32_t(vP[q & 0x7FFFu]);
+            (void)vP;
+            for (uint32_t h = uint32_t(tid) << kNS; h < (nodes << kNS); h += uint32_t(C::NT) << kNS) {
+                const uint32_t p = *nslot(P, h);
+                const uint32_t q = (p & kRoot) ? p : uint32_t(*nslot(P, p & 0x7FFFu));
+                uint32_t r = (q & kRoot) ? q : uint32_t(*nslot(P, q & 0x7FFFu));
                 if (!(r & kRoot)) {
                     do {
                         mc.step();
-                        r = vP[r];
+                        r = *nslot(P, r);
                     } while (!(r & kRoot));
                 }
-                if (!(p & kRoot)) vP[id] = node_t(r);
+                if (!(p & kRoot)) *nslot(P, h) = node_t(r);
             }
         }
         const uint32_t nf = FR[0];
@@ -1207,7 +1214,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             const uint32_t x = BN[i];
             uint32_t v = kBG;
             if (x != 0xFFFFu) {
-                const uint32_t code = P[x];
+                const uint32_t code = *nslot(P, x);
                 if (code & kSeam) v = FR[1 + (code & kCode)];
             }
             wt[C::W_REC + i] = v;
