@@ -1022,14 +1022,15 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 const uint32_t top_root = tfirst & ~seg_back(firstm, rss, rse);
                 const uint32_t rb = bs[k] & ~seg_back(tfirst, rss, rse);
                 uint32_t mk = firstm | top_root | rb;
-                const uint32_t c0 = kRoot | rowpos0;
+                const uint32_t c0 = kRoot | rowpos0, c1 = c0 + uint32_t(C::TW);
+                const uint32_t uh = (upfx[k] - 1u) << kNS;  // + (starts at or below the bit above) << kNS
                 node_t* dst = P + pfx[k];
                 while (mk) {
                     const uint32_t lb = mk & (0u - mk);
-                    const uint32_t a = 31u - __clz(lb);
+                    const uint32_t code = ((rb & lb) ? c1 : c0) + (31u - __clz(lb));
+                    const uint32_t up = uh + (uint32_t(__popc(ubs[k] << __clz(lb))) << kNS);
+                    *dst++ = node_t((firstm & lb) ? up : code);
                     mk ^= lb;
-                    const uint32_t code = c0 + a + ((rb & lb) ? uint32_t(C::TW) : 0u);
-                    *dst++ = node_t((firstm & lb) ? node_of(upfx[k], ubs[k], a) << kNS : code);
                 }
             }
             const bool last_has_top = bs[k] && (tfirst & (0xFFFFFFFFu << (31u - __clz(bs[k]))));
@@ -1072,10 +1073,16 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 uint32_t* dst = UL + (inc - cu);
 #pragma unroll
                 for (int k = 0; k < WPL; ++k) {
+                    // pair of handles {this band's node, the node above} of every
+                    // remaining overlap bit (node_of as a popcount of the starts
+                    // shifted up to the bit, on handle bases)
+                    const uint32_t ph = (pfx[k] - 1u) << kNS, uhh = ((upfx[k] - 1u) << kNS) << 16;
                     while (U[k]) {
-                        const uint32_t b = lowbit(U[k]);
-                        U[k] &= U[k] - 1;
-                        *dst++ = (node_of(pfx[k], bs[k], b) << kNS) | (node_of(upfx[k], ubs[k], b) << (16 + kNS));
+                        const uint32_t lb = U[k] & (0u - U[k]);
+                        const uint32_t sh = __clz(lb);
+                        *dst++ = (ph + (uint32_t(__popc(bs[k] << sh)) << kNS)) +
+                                 (uhh + (uint32_t(__popc(ubs[k] << sh)) << (16 + kNS)));
+                        U[k] ^= lb;
                     }
                 }
             }
