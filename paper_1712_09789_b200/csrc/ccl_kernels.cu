@@ -334,6 +334,19 @@ __device__ __forceinline__ uint32_t word_starts(uint32_t m, uint32_t lm) {
     return m & ~((m << 1) | cont);
 }
 
+// Inclusive warp scan: shfl.up hands back whether the source lane exists, so
+// each step is a shuffle and a predicated add (no lane compare and select).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+        asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+            "@p add.u32 %0, %0, t;\n\t}"
+            : "+r"(v)
+            : "r"(d));
+    return v;
+}
+
 // Raster-order node prefix of every row word of the tile.  Each lane owns
 // word (row, wx) with `cnt` node starts; CNT is scratch for the counts.
 // Returns the number of nodes that start before this word; *total = nodes in
@@ -350,12 +363,7 @@ __device__ __forceinline__ uint32_t tile_prefix(uint32_t cnt, uint32_t* CNT, uin
         left += (w < wx) ? c : 0u;
         rowtot += c;
     }
-    uint32_t inc = rowtot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
+    const uint32_t inc = warp_incl_scan(rowtot);
     uint32_t band = 0, tot;
     if (C::WY == 1) {
         tot = __shfl_sync(0xffffffffu, inc, 31);
@@ -1061,12 +1069,7 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
             uint32_t cu = 0;
 #pragma unroll
             for (int k = 0; k < WPL; ++k) cu += __popc(U[k]);
-            uint32_t inc = cu;
-#pragma unroll
-            for (int j = 1; j < 32; j <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, j);
-                if (lane >= j) inc += y;
-            }
+            const uint32_t inc = warp_incl_scan(cu);
             const bool fits = inc <= uint32_t(A::UL_CAP);
             nul = __reduce_max_sync(0xffffffffu, fits ? inc : 0u);
             if (fits) {
