@@ -1032,12 +1032,13 @@ __device__ __forceinline__ void local_band_tiles(const CUtensorMap* tmap, const 
                 uint32_t mk = firstm | top_root | rb;
                 const uint32_t c0 = kRoot | rowpos0, c1 = c0 + uint32_t(C::TW);
                 const uint32_t uh = (upfx[k] - 1u) << kNS;  // + (starts at or below the bit above) << kNS
-                node_t* dst = P + pfx[k];
+                uint32_t hd = pfx[k] << kNS;  // handle of the next node
                 while (mk) {
                     const uint32_t lb = mk & (0u - mk);
                     const uint32_t code = ((rb & lb) ? c1 : c0) + (31u - __clz(lb));
                     const uint32_t up = uh + (uint32_t(__popc(ubs[k] << __clz(lb))) << kNS);
-                    *dst++ = node_t((firstm & lb) ? up : code);
+                    *nslot(P, hd) = node_t((firstm & lb) ? up : code);
+                    hd += 1u << kNS;
                     mk ^= lb;
                 }
             }
