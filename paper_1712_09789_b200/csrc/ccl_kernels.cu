@@ -1495,8 +1495,13 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
         const TileId ti = walk.cur;
         const uint32_t x0 = ti.tx * C::TW, y0 = ti.ty * C::TH;
 
+        // label of a root code: a seam root's resolved label, else the global
+        // raster index of its tile position (pos_gidx as one multiply-add:
+        // y * W + x = pos + (pos / TW) * (W - TW))
+        const uint32_t gbase = (g.row0 + y0) * g.W + x0, wm = g.W - uint32_t(C::TW);
         auto lab_of = [&](uint32_t v) -> uint32_t {
-            return (v & kSeam) ? FT[v & kCode] : pos_gidx<C>(v & kCode, x0, y0, g);
+            const uint32_t pos = v & kCode;
+            return (v & kSeam) ? FT[pos] : gbase + pos + (pos >> __builtin_ctz(C::TW)) * wm;
         };
         if (TMA_ST) {  // this warp's previous TMA stores must have read the staging tiles
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1527,6 +1532,7 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
             uint8_t* row0 = stg + (r0 & 31) * 128;
             uint8_t* row1 = stg + (r1 & 31) * 128;
             const int sw0 = r0 & 7, sw1 = r1 & 7;
+            const uint32_t swz0 = uint32_t(sw0) << 4;  // 128B swizzle: 16-byte chunk index ^= row & 7
             const uint32_t tm = M[r0 * C::WPR + wc], um = M[r1 * C::WPR + wc];
             const uint32_t st = BSt[b * C::WPR + wc];
             const uint32_t pfx = PF16[b * C::WPR + wc];
@@ -1541,7 +1547,7 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
                     const uint32_t bb = ((__ffs(tt) - 1) + rot) & 31u;
                     tt &= tt - 1;
                     const uint32_t e = pfx + __popc(st & ((1u << bb) - 1u));
-                    *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(tbl[e]);
+                    *reinterpret_cast<uint32_t*>(row0 + ((bb << 2) ^ swz0)) = lab_of(tbl[e]);
                 }
             } else {
                 const uint16_t* e = tbl + pfx;
@@ -1549,7 +1555,7 @@ __device__ __forceinline__ void final_tiles(const CUtensorMap* tmap, uint32_t* L
                 while (tt) {
                     const uint32_t bb = __ffs(tt) - 1;
                     tt &= tt - 1;
-                    *reinterpret_cast<uint32_t*>(row0 + ((((bb >> 2) ^ sw0) << 4) | ((bb & 3) << 2))) = lab_of(*e++);
+                    *reinterpret_cast<uint32_t*>(row0 + ((bb << 2) ^ swz0)) = lab_of(*e++);
                 }
             }
             uint4 vv[8];  // all read-backs first: the stores below may not be hoisted over
