@@ -1,24 +1,32 @@
 // ccl_kernels.cu — the hand-written sm_100a kernels of the labeler.
 //
-//   (a)+(b)+(c)  k_local  : TMA-stage a TW x TH tile, foreground row words,
-//                           word-level run detection (coarse row scan) with
-//                           runs that continue across 32-px words kept as ONE
-//                           node, COMPACT node ids in tile raster order
-//                           (prefix counts), coarse column links, smem
-//                           min-union refinement, and an id-ordered flatten
-//                           (unification).  Exports, per tile, a run table
-//                           (one u16 per node: local root position, or the
-//                           rank of a seam-touching root), the row-word masks
-//                           and the seam-touching root list; writes the tile's
-//                           seam pixels and registers the seam-touching roots
-//                           as nodes of the global forest in the label buffer.
-//   (d)          k_seams  : boundary-only pass (Algorithm 2): one thread per
-//                           interior tile-seam pixel pair, global atomicMin
-//                           union-find directly in the label buffer.
-//   (e)          k_final  : resolves each seam-touching root ONCE through the
-//                           global forest, expands the run table to pixels and
-//                           writes every label exactly once (swizzled TMA
-//                           stores).  It never re-reads the image.
+//   (a)+(b)+(c)  k_local_band (C2FL, the default)  : persistent, one 128x64
+//                           tile per CTA at a time, TMA-staged.  Lane = a 2-row
+//                           band of one 32-px word: band runs from bit masks,
+//                           COMPACT node ids in tile raster order (prefix
+//                           counts), one coarse loop over per-run marker bits
+//                           (links to the band above / root codes), a
+//                           pointer-jump round where runs mostly link, shared-
+//                           memory min-union refinement over node HANDLES (the
+//                           entries' byte offsets), seam-touching roots registered
+//                           in the compact global forest, then a node table of
+//                           root codes.  Hands off, per tile: row masks, band
+//                           prefixes / starts, the table, the seam-root list and
+//                           the seam records (root of every border pixel).
+//                k_local<VAR> : the same on row runs for the RC2FL / CC2FL / NC2FL
+//                           variants (coarse scans per the reference's variant).
+//   (d)          k_seams  : boundary-only pass (Algorithm 2) over the seam
+//                           records: one warp per four 32-pair chunks, one union
+//                           per distinct pair, min-key CAS union-find in the
+//                           compact L2-resident forest.
+//   (d2)         k_resolve: each tile's seam-touching roots climb to their class
+//                           root once; the final labels go into the tile's list.
+//   (e)          k_final  : persistent 3-stage pipeline: expands every band run
+//                           to its two rows in a 128B-swizzled staging tile and
+//                           writes every label exactly once (TMA stores).  It
+//                           never re-reads the image.
+//   (d), (d2), (e) are programmatic dependent launches of (a); the chain is
+//   graph-replayed by the C-ABI.
 //
 // Node ids are assigned in tile raster order, so the min-id root of a class is
 // its min raster position (forest.hpp:44-111 invariant parent <= self), which
