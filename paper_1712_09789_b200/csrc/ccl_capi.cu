@@ -424,7 +424,7 @@ ccl_status ccl_label_batch(ccl_ctx* ctx, const uint8_t* d_frames, size_t img_pit
     ctx->last_split = false;
     CCL_CHECK(cudaEventRecord(ctx->ev[0], st));
     CCL_CHECK(cudaStreamWaitEvent(s2, ctx->ev[0], 0));  // inputs / previous work on the caller's stream
-    const int acap = env_int("CCL_PIPE_A", 8), ecap = env_int("CCL_PIPE_E", 3);  // tuned: scripts/batch_sweep.py
+    const int acap = env_int("CCL_PIPE_A", 6), ecap = env_int("CCL_PIPE_E", 4);  // tuned: scripts/batch_sweep.py (r2n)
     for (uint32_t j = 0; j < nchunks; ++j) {
         const uint32_t f0 = j * chunk, nj = std::min(chunk, n - f0);
         cclk::LaunchArgs a{};

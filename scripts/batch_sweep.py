@@ -44,5 +44,6 @@ def run(tag, **env):
 run("no pipeline", CCL_PIPE=0)
 import itertools
 for tiles in [int(x) for x in os.environ.get("SWEEP_TILES", "12288,16384,24576").split(",")]:
-    for a, e in ((8, 2), (8, 3), (7, 3), (9, 2), (10, 2), (6, 4), (4, 4), (5, 3), (9, 1), (10, 1), (7, 2), (6, 2)):
+    pairs = os.environ.get("SWEEP_PAIRS", "8:2,8:3,7:3,9:2,10:2,6:4,4:4,5:3,9:1,10:1,7:2,6:2")
+    for a, e in [tuple(int(v) for v in p.split(":")) for p in pairs.split(",")]:
         run(f"tiles {tiles} a{a} e{e}", CCL_PIPE_TILES=tiles, CCL_PIPE_A=a, CCL_PIPE_E=e)
